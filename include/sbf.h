@@ -1,0 +1,193 @@
+/*
+ * sbf.h — C ABI of the B200-native shiftable bilateral filter (sm_100a).
+ *
+ * Drop-in boundary for the hot path of the reference package `shiftbf`
+ * (arXiv 1203.5128).  Plain pointers and sizes only: no torch types.  All
+ * device pointers are caller-owned; the library never frees them.  Every
+ * call is stream-ordered and reentrant (no global mutable state besides a
+ * thread-local error string).  Status codes mirror the reference CLI exit
+ * codes (reference cli.py:309-314) and map onto its exception types
+ * (reference errors.py:4-25):
+ *
+ *   SBF_OK               0
+ *   SBF_ERR_INVALID      2  -> InvalidParameterError
+ *   SBF_ERR_UNSUPPORTED  4  -> UnsupportedOrderError (order/term capacity)
+ *   SBF_ERR_CUDA         5  -> RuntimeError (launch or device fault)
+ *   SBF_ERR_WORKSPACE    6  -> InvalidParameterError (workspace too small)
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/shiftbf):
+ *   sbf_extended_box_params   spatial.py:81-100   extended_box_params
+ *   sbf_support_radius        spatial.py:185-194  support_radius
+ *   sbf_select_plan           kernels.py:166-195  select_plan (host twin of K2)
+ *   sbf_truncation_index_exact kernels.py:131-149
+ *   sbf_truncation_index_chernoff kernels.py:152-163
+ *   sbf_local_range           maxfilter.py:41-61  max_filter_2d + compute_T
+ *                             (_core running_max_lines, _fastcore.pyx:16-58)
+ *   sbf_plan_device           kernels.py:166-227  select_plan +
+ *                             raised_cosine_expansion, on the device
+ *   sbf_filter                bilateral.py:140-164 _accumulate_cosine_terms
+ *                             + spatial.py:108-139 iterated_box_gaussian /
+ *                             :65-78 box_filter (+ _core window_sum_lines,
+ *                             _fastcore.pyx:61-86) + bilateral.py:242-254
+ *                             _divide_with_fallback
+ *   sbf_shiftable_bf          bilateral.py:117-137 shiftable_bf (device bufs)
+ *   sbf_shiftable_bf_host     bilateral.py:117-137 shiftable_bf (host bufs)
+ */
+#ifndef SBF_H_
+#define SBF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SBF_ABI_VERSION 1
+
+#define SBF_OK 0
+#define SBF_ERR_INVALID 2
+#define SBF_ERR_UNSUPPORTED 4
+#define SBF_ERR_CUDA 5
+#define SBF_ERR_WORKSPACE 6
+
+/* element types of image buffers */
+#define SBF_F32 0
+#define SBF_F64 1
+
+/* truncation rules (kernels.py:173-192) */
+#define SBF_RULE_AUTO 0
+#define SBF_RULE_EXACT 1
+#define SBF_RULE_CHERNOFF 2
+#define SBF_RULE_NONE 3
+
+/* spatial modes (spatial.py:24-42) */
+#define SBF_SPATIAL_ITERATED 0
+#define SBF_SPATIAL_BOX 1
+
+/* precision modes of the term kernel */
+#define SBF_PREC_FP32 0   /* fp32 phases, sums and accumulators (8-bit-scale images) */
+#define SBF_PREC_HDR 1    /* fp64 running sums and num/den accumulators (16-bit scale) */
+
+/* plan flags */
+#define SBF_PLAN_N_AMBIGUOUS 1     /* ceil(0.405 x^2) changes within +-2 ulp of x^2 */
+#define SBF_PLAN_EXACT_BIGINT 2    /* exact rule resolved by the multi-limb path */
+#define SBF_PLAN_TERMS_TRUNCATED 4 /* term table capacity exceeded (status set) */
+
+typedef struct sbf_plan {
+  double T;        /* dynamic range the plan was built for */
+  double sigma_r;
+  double epsilon;
+  double gamma;    /* 1 / (sqrt(N) sigma_r) */
+  int32_t N;       /* kernel order */
+  int32_t M;       /* terms dropped from each tail */
+  int32_t K;       /* folded terms n in [M, floor(N/2)] */
+  int32_t K_eval;  /* folded terms with non-zero weight (evaluated) */
+  int32_t flags;
+  int32_t status;  /* SBF_OK or an error code */
+  int32_t pad0, pad1;
+} sbf_plan;        /* 64 bytes */
+
+typedef struct sbf_term {
+  double scale;    /* d_n, or 2 d_n for a folded +-pair (bilateral.py:154) */
+  double freq;     /* omega_n = (2n - N) / (sqrt(N) sigma_r) */
+  double turns;    /* omega_n / (2 pi) */
+  int32_t index;   /* n */
+  int32_t pad;
+} sbf_term;        /* 32 bytes */
+
+typedef struct sbf_spatial {
+  int32_t mode;    /* SBF_SPATIAL_* */
+  int32_t passes;  /* 1 for box */
+  int32_t r;       /* per-pass integer radius */
+  int32_t pad;
+  double alpha;    /* endpoint weight (0 for box) */
+  double sigma_s;  /* informational */
+} sbf_spatial;
+
+/* ---- library info ---- */
+int sbf_abi_version(void);
+const char* sbf_last_error(void);
+int sbf_device_count(int* count);
+
+/* ---- host scalar logic (identical code runs on the device in K2) ---- */
+int sbf_extended_box_params(double sigma_s, int passes, int* r, double* alpha);
+int sbf_support_radius(const sbf_spatial* sp, int* radius);
+int sbf_truncation_index_exact(int N, double epsilon, int* M);
+int sbf_truncation_index_chernoff(int N, double epsilon, double log_2_over_eps, int* M);
+int sbf_order_threshold(double T, double sigma_r, int* N);
+int sbf_select_plan(double T, double sigma_r, double epsilon, int rule,
+                    double log_2_over_eps, sbf_plan* out);
+
+/* ---- device entry points (all pointers device memory, stream = cudaStream_t) ---- */
+
+/* Workspace (bytes) needed by sbf_local_range for an H x W image. */
+size_t sbf_local_range_workspace(int64_t H, int64_t W, int dtype);
+
+/* Max filter over the clamped (2R+1)^2 window and T = max(M - f) in fp64.
+ * f: H x W row-major (row pitch `ld` elements), dtype SBF_F32/SBF_F64.
+ * T and the image statistics are computed over buffer rows [t_lo, t_hi)
+ * (row strips with halos: pass the interior rows).  M_out (nullable) gets
+ * the max-filter image in the input dtype.  stats_dev (>= 4 doubles):
+ * [0] = T, [1] = min f, [2] = max f, [3] = centre used by sbf_filter. */
+int sbf_local_range(const void* f, int dtype, int64_t H, int64_t W, int64_t ld,
+                    int R, int64_t t_lo, int64_t t_hi, void* M_out,
+                    double* stats_dev, void* ws, size_t ws_bytes, void* stream);
+
+/* Plan on the device from T = *T_dev (or fixed_T if use_fixed != 0):
+ * N, M, folded term table sorted largest weight first. */
+int sbf_plan_device(const double* T_dev, int use_fixed, double fixed_T,
+                    double sigma_r, double epsilon, int rule,
+                    double log_2_over_eps, sbf_plan* plan_dev,
+                    sbf_term* terms_dev, int terms_cap, void* stream);
+
+/* Workspace (bytes) for sbf_filter. */
+size_t sbf_filter_workspace(int64_t rows_out, int64_t W, const sbf_spatial* sp,
+                            int precision);
+
+/* The fused shiftable filter for output rows [out_lo, out_hi) of a buffer
+ * holding global image rows [row0, row0 + H) of an image of global height
+ * img_H (border renormalisation only at true image borders).  The buffer
+ * must include every row within the spatial support of the output rows.
+ * out: (out_hi - out_lo) x W, pitch W, dtype out_dtype.
+ * stats_dev: from sbf_local_range ([3] = centre).  fallback_dev: one
+ * unsigned long long counter (accumulated). */
+int sbf_filter(const void* f, int dtype, int64_t H, int64_t W, int64_t ld,
+               int64_t row0, int64_t img_H, int64_t out_lo, int64_t out_hi,
+               const sbf_spatial* sp, const sbf_plan* plan_dev,
+               const sbf_term* terms_dev, const double* stats_dev,
+               int precision, void* out, int out_dtype,
+               unsigned long long* fallback_dev, void* ws, size_t ws_bytes,
+               void* stream);
+
+/* Whole pipeline (K1 -> K2 -> K3 -> K4) on device buffers; no host sync.
+ * fixed_T < 0 means "compute T with window radius R". */
+size_t sbf_shiftable_bf_workspace(int64_t H, int64_t W, int dtype,
+                                  const sbf_spatial* sp, int precision,
+                                  int terms_cap);
+int sbf_shiftable_bf(const void* f, int dtype, int64_t H, int64_t W,
+                     const sbf_spatial* sp, int R, double fixed_T,
+                     double sigma_r, double epsilon, int rule,
+                     double log_2_over_eps, int precision, void* out,
+                     int out_dtype, sbf_plan* plan_dev, double* stats_dev,
+                     unsigned long long* fallback_dev, int terms_cap,
+                     void* ws, size_t ws_bytes, void* stream);
+
+/* Host-buffer convenience (copies in, runs, copies out, synchronises).
+ * Output is float64 like the reference.  plan_out / fallback_out on host. */
+int sbf_shiftable_bf_host(const double* f_host, int64_t H, int64_t W,
+                          const sbf_spatial* sp, int R, double fixed_T,
+                          double sigma_r, double epsilon, int rule,
+                          double log_2_over_eps, int precision,
+                          double* out_host, sbf_plan* plan_out,
+                          unsigned long long* fallback_out);
+
+/* Divide/fallback epilogue on caller buffers (bilateral.py:242-254), fp64. */
+int sbf_divide_with_fallback(const double* num, const double* den,
+                             const double* fallback, int64_t n, double* out,
+                             unsigned long long* count_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SBF_H_ */

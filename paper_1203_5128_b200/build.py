@@ -1,0 +1,112 @@
+"""Build libsbf.so (sm_100a) in-tree with nvcc; no torch extension machinery.
+
+    python -m paper_1203_5128_b200.build [--full|--min] [-j N]
+
+Each specialised K3 instantiation (r, passes, precision mode) is its own
+object so the build parallelises.  The instantiation list is written to
+csrc/sbf_terms_list.inc, which the dispatcher includes.
+"""
+
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "_build")
+LIB = os.path.join(HERE, "libsbf.so")
+INCLUDE = os.path.join(os.path.dirname(HERE), "include")
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+         "-I", INCLUDE, "-I", CSRC]
+
+SOURCES = ["sbf_api.cu", "sbf_plan.cu", "sbf_local_range.cu", "sbf_generic.cu"]
+
+
+def instantiations(kind: str):
+    """(r, passes, mode) triples with a specialised K3 kernel."""
+    if kind == "min":
+        return [(2, 3, 0), (4, 3, 0), (5, 3, 0), (7, 3, 1)]
+    out = []
+    for r in range(0, 13):
+        out.append((r, 3, 0))
+    for r in range(1, 13):
+        out.append((r, 1, 0))
+    for r in range(0, 13):
+        out.append((r, 3, 1))
+    return out
+
+
+def _newer(target, deps):
+    if not os.path.exists(target):
+        return False
+    t = os.path.getmtime(target)
+    return all(os.path.getmtime(d) <= t for d in deps)
+
+
+def _headers():
+    hs = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".cuh", ".h", ".inc"))]
+    hs.append(os.path.join(INCLUDE, "sbf.h"))
+    return hs
+
+
+def _compile(args):
+    src, obj, defs = args
+    deps = [src] + _headers()
+    if _newer(obj, deps):
+        return obj, 0, ""
+    cmd = [NVCC] + ARCH + FLAGS + defs + ["-c", src, "-o", obj]
+    p = subprocess.run(cmd, capture_output=True, text=True)
+    return obj, p.returncode, p.stdout + p.stderr
+
+
+def build(kind: str = "full", jobs: int | None = None, verbose: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    inst = instantiations(kind)
+    inc = os.path.join(CSRC, "sbf_terms_list.inc")
+    text = "".join(f"SBF_X({r}, {p}, {m})\n" for r, p, m in inst)
+    if not os.path.exists(inc) or open(inc).read() != text:
+        with open(inc, "w") as fh:
+            fh.write(text)
+    jobs_list = [(os.path.join(CSRC, s), os.path.join(OBJ, s.replace(".cu", ".o")), [])
+                 for s in SOURCES]
+    for r, p, m in inst:
+        jobs_list.append((os.path.join(CSRC, "sbf_terms_inst.cu"),
+                          os.path.join(OBJ, f"terms_r{r}_p{p}_m{m}.o"),
+                          [f"-DSBF_R={r}", f"-DSBF_P={p}", f"-DSBF_M={m}"]))
+    jobs = jobs or max(1, os.cpu_count() or 1)
+    failed = []
+    with cf.ThreadPoolExecutor(jobs) as ex:
+        for obj, rc, out in ex.map(_compile, jobs_list):
+            if rc != 0:
+                failed.append((obj, out))
+            elif verbose and out.strip():
+                print(out)
+    if failed:
+        for obj, out in failed:
+            sys.stderr.write(f"--- {obj}\n{out}\n")
+        raise RuntimeError(f"nvcc failed for {len(failed)} object(s)")
+    objs = [j[1] for j in jobs_list]
+    if not _newer(LIB, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
+        p = subprocess.run(cmd, capture_output=True, text=True)
+        if p.returncode != 0:
+            raise RuntimeError("link failed:\n" + p.stdout + p.stderr)
+    return LIB
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    g = ap.add_mutually_exclusive_group()
+    g.add_argument("--full", action="store_true")
+    g.add_argument("--min", action="store_true")
+    ap.add_argument("-j", type=int, default=None)
+    ap.add_argument("-v", action="store_true")
+    a = ap.parse_args()
+    print(build("min" if a.min else "full", a.j, a.v))

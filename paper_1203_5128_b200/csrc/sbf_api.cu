@@ -1,0 +1,443 @@
+// C ABI (include/sbf.h): validation, dispatch, workspace layout, epilogue K4.
+#include <stdarg.h>
+#include <string.h>
+
+#include <vector>
+
+#include "sbf_common.cuh"
+#include "sbf_plan_logic.cuh"
+#include "sbf_terms.cuh"
+
+namespace sbf {
+
+static thread_local char g_err[512];
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int launch_generic_terms(const FilterLaunch& a, double* nd);
+
+// ---- registry of specialised K3 instantiations (generated list) ----
+#define SBF_X(R, P, M) TermsEntry terms_entry_##R##_##P##_##M();
+#include "sbf_terms_list.inc"
+#undef SBF_X
+
+static const std::vector<TermsEntry>& registry() {
+  static const std::vector<TermsEntry> reg = {
+#define SBF_X(R, P, M) terms_entry_##R##_##P##_##M(),
+#include "sbf_terms_list.inc"
+#undef SBF_X
+  };
+  return reg;
+}
+
+static const TermsEntry* find_entry(const sbf_spatial& sp, int precision) {
+  const int passes = sp.mode == SBF_SPATIAL_BOX ? 1 : sp.passes;
+  for (const auto& e : registry())
+    if (e.r == sp.r && e.passes == passes && e.mode == precision) return &e;
+  return nullptr;
+}
+
+static int sm_count() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 148;
+  }
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    return 148;
+  }
+  return n;
+}
+
+// strips x bands x term-groups; groups chosen so the grid fills whole waves
+static void choose_geometry(const TermsEntry& e, int64_t rows_out, int64_t W, TermGeom* g) {
+  int halo, wc, threads, bps;
+  e.geom(&halo, &wc, &threads, &bps);
+  g->halo = halo;
+  g->wc = wc;
+  g->threads = threads;
+  g->halo_w = 128;
+  g->rows = threads / 4;
+  g->nstrips = (int)((W + wc - 1) / wc);
+  const int64_t band = rows_out < 512 ? rows_out : 512;
+  g->band = (int)(band < 1 ? 1 : band);
+  g->nbands = (int)((rows_out + g->band - 1) / g->band);
+  const double slots = (double)sm_count() * bps;
+  const double base = (double)g->nstrips * g->nbands;
+  int best = 1;
+  double best_eff = -1.0;
+  for (int G = 1; G <= 32; ++G) {
+    const double ctas = base * G;
+    const double waves = ceil(ctas / slots);
+    // a term group costs 1/G of the terms; more than ~4 waves gains nothing
+    const double eff = ctas / (waves * slots);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = G;
+    }
+    if (ctas > 4 * slots) break;
+  }
+  g->groups = best;
+  g->smem = e.smem(g->band);
+}
+
+static bool spatial_coeffs(const sbf_spatial& sp, int* r, int* passes, double* alpha) {
+  if (sp.mode == SBF_SPATIAL_BOX) {
+    *r = sp.r;
+    *passes = 1;
+    *alpha = 0.0;
+  } else {
+    *r = sp.r;
+    *passes = sp.passes;
+    *alpha = sp.alpha;
+  }
+  return *r >= 0 && *passes >= 1 && *alpha >= 0.0 && *alpha < 1.0;
+}
+
+size_t filter_ws(int64_t rows_out, int64_t W, const sbf_spatial* sp, int precision) {
+  const TermsEntry* e = find_entry(*sp, precision);
+  const size_t pair = precision == SBF_PREC_HDR ? 16 : 8;
+  if (!e) return align_up((size_t)(rows_out * W) * 16);  // generic: one fp64 accumulator
+  TermGeom g;
+  choose_geometry(*e, rows_out, W, &g);
+  return align_up((size_t)g.groups * (size_t)(rows_out * W) * pair);
+}
+
+// ---------------------------- K4 epilogue ----------------------------
+template <typename ACC, typename FT, typename OT>
+__global__ void epilogue_kernel(const ACC* __restrict__ nd, int groups, int64_t gstride,
+                                const sbf_plan* __restrict__ plan, int64_t rows, int64_t W,
+                                const FT* __restrict__ f, int64_t ld, int64_t out_lo,
+                                const double* __restrict__ stats, OT* __restrict__ out,
+                                unsigned long long* __restrict__ fallback) {
+  const int used = min(groups, plan->K_eval);
+  const double center = stats[3];
+  const int64_t n = rows * W;
+  unsigned long long bad_count = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double num = 0.0, den = 0.0;
+    for (int g = 0; g < used; ++g) {
+      num += (double)nd[2 * (g * gstride + i)];
+      den += (double)nd[2 * (g * gstride + i) + 1];
+    }
+    const int64_t y = i / W, x = i - y * W;
+    const bool bad = !(den > 0.0);  // bilateral.py:244 (NaN counts as bad)
+    const double o = bad ? (double)f[(out_lo + y) * ld + x] : num / den + center;
+    out[i] = (OT)o;
+    bad_count += bad ? 1 : 0;
+  }
+  for (int o = 16; o; o >>= 1) bad_count += __shfl_xor_sync(0xffffffffu, bad_count, o);
+  if ((threadIdx.x & 31) == 0 && bad_count) atomicAdd(fallback, bad_count);
+}
+
+template <typename ACC>
+static int launch_epilogue(const FilterLaunch& a, const ACC* nd, int groups, int64_t gstride) {
+  const int64_t rows = a.out_hi - a.out_lo;
+  const int64_t n = rows * a.W;
+  const unsigned grid = (unsigned)smin<int64_t>((n + 255) / 256, 148 * 8);
+#define SBF_EPI(FT, OT)                                                                      \
+  epilogue_kernel<ACC, FT, OT><<<grid, 256, 0, a.stream>>>(                                  \
+      nd, groups, gstride, a.plan, rows, a.W, static_cast<const FT*>(a.f), a.ld, a.out_lo, \
+      a.stats, static_cast<OT*>(a.out), a.fallback)
+  if (a.dtype == SBF_F32 && a.out_dtype == SBF_F32) SBF_EPI(float, float);
+  else if (a.dtype == SBF_F32 && a.out_dtype == SBF_F64) SBF_EPI(float, double);
+  else if (a.dtype == SBF_F64 && a.out_dtype == SBF_F32) SBF_EPI(double, float);
+  else SBF_EPI(double, double);
+#undef SBF_EPI
+  SBF_CHECK_LAUNCH();
+  return SBF_OK;
+}
+
+int launch_filter(const FilterLaunch& a) {
+  int r, passes;
+  double alpha;
+  SBF_REQUIRE(a.f && a.out && a.plan && a.terms && a.stats && a.fallback, SBF_ERR_INVALID,
+              "null pointer");
+  SBF_REQUIRE(a.dtype == SBF_F32 || a.dtype == SBF_F64, SBF_ERR_INVALID, "bad dtype");
+  SBF_REQUIRE(a.out_dtype == SBF_F32 || a.out_dtype == SBF_F64, SBF_ERR_INVALID, "bad out dtype");
+  SBF_REQUIRE(a.H >= 1 && a.W >= 1 && a.ld >= a.W, SBF_ERR_INVALID, "bad image shape");
+  SBF_REQUIRE(a.out_lo >= 0 && a.out_hi <= a.H && a.out_lo < a.out_hi, SBF_ERR_INVALID,
+              "bad output row range");
+  SBF_REQUIRE(a.row0 >= 0 && a.row0 + a.H <= a.img_H, SBF_ERR_INVALID, "bad global row range");
+  SBF_REQUIRE(spatial_coeffs(a.sp, &r, &passes, &alpha), SBF_ERR_INVALID, "bad spatial mode");
+  SBF_REQUIRE(a.precision == SBF_PREC_FP32 || a.precision == SBF_PREC_HDR, SBF_ERR_INVALID,
+              "bad precision mode");
+  // the buffer must hold every row within the spatial support of the outputs
+  const int64_t sup = (int64_t)passes * (r + 1);
+  SBF_REQUIRE((a.out_lo - sup >= 0 || a.row0 == 0) &&
+                  (a.out_hi + sup <= a.H || a.row0 + a.H == a.img_H),
+              SBF_ERR_INVALID, "row strip lacks a halo of %lld rows", (long long)sup);
+  const int64_t rows_out = a.out_hi - a.out_lo;
+  SBF_REQUIRE(a.H <= INT32_MAX && a.W <= INT32_MAX, SBF_ERR_INVALID, "image too large");
+
+  const TermsEntry* e = find_entry(a.sp, a.precision);
+  if (!e) {
+    const size_t need = align_up((size_t)(rows_out * a.W) * 16);
+    SBF_REQUIRE(a.ws && a.ws_bytes >= need, SBF_ERR_WORKSPACE, "filter workspace too small");
+    double* nd = static_cast<double*>(a.ws);
+    int rc = launch_generic_terms(a, nd);
+    if (rc != SBF_OK) return rc;
+    return launch_epilogue<double>(a, nd, 1, rows_out * a.W);
+  }
+  TermGeom g;
+  choose_geometry(*e, rows_out, a.W, &g);
+  const size_t pair = a.precision == SBF_PREC_HDR ? 16 : 8;
+  const size_t need = align_up((size_t)g.groups * (size_t)(rows_out * a.W) * pair);
+  SBF_REQUIRE(a.ws && a.ws_bytes >= need, SBF_ERR_WORKSPACE,
+              "filter workspace too small (%zu < %zu)", a.ws_bytes, need);
+  TermParams p;
+  memset(&p, 0, sizeof(p));
+  p.f = a.f;
+  p.ld = a.ld;
+  p.f64 = a.dtype == SBF_F64;
+  p.H = (int)a.H;
+  p.W = (int)a.W;
+  p.row0 = a.row0;
+  p.img_H = a.img_H;
+  p.out_lo = (int)a.out_lo;
+  p.out_hi = (int)a.out_hi;
+  p.band = g.band;
+  p.nstrips = g.nstrips;
+  p.nbands = g.nbands;
+  p.groups = g.groups;
+  p.r = r;
+  p.alpha = (float)alpha;
+  const double cint = 2.0 * r + 1.0 + 2.0 * alpha;
+  p.ad = (1.0 - alpha) / cint;
+  p.bd = alpha / cint;
+  p.a = (float)p.ad;
+  p.b = (float)p.bd;
+  p.plan = a.plan;
+  p.terms = a.terms;
+  p.stats = a.stats;
+  p.nd = a.ws;
+  p.nd_group_stride = rows_out * a.W;
+  int rc = e->launch(p, a.stream);
+  if (rc != SBF_OK) return rc;
+  if (a.precision == SBF_PREC_HDR)
+    return launch_epilogue<double>(a, static_cast<const double*>(a.ws), g.groups, rows_out * a.W);
+  return launch_epilogue<float>(a, static_cast<const float*>(a.ws), g.groups, rows_out * a.W);
+}
+
+}  // namespace sbf
+
+using namespace sbf;
+
+static cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+int sbf_abi_version(void) { return SBF_ABI_VERSION; }
+const char* sbf_last_error(void) { return sbf::g_err; }
+
+int sbf_device_count(int* count) {
+  if (!count) return SBF_ERR_INVALID;
+  SBF_CHECK_CUDA(cudaGetDeviceCount(count));
+  return SBF_OK;
+}
+
+// number of specialised K3 instantiations and their (r, passes, mode)
+int sbf_num_specialisations(void) { return (int)registry().size(); }
+int sbf_specialisation(int i, int* r, int* passes, int* mode) {
+  if (i < 0 || i >= (int)registry().size()) return SBF_ERR_INVALID;
+  *r = registry()[i].r;
+  *passes = registry()[i].passes;
+  *mode = registry()[i].mode;
+  return SBF_OK;
+}
+
+// launch geometry the library would use (for reports / tests)
+int sbf_filter_geometry(int64_t rows_out, int64_t W, const sbf_spatial* sp, int precision,
+                        int* out7) {
+  const TermsEntry* e = sp ? find_entry(*sp, precision) : nullptr;
+  if (!e || !out7) return SBF_ERR_UNSUPPORTED;
+  TermGeom g;
+  choose_geometry(*e, rows_out, W, &g);
+  out7[0] = g.halo;
+  out7[1] = g.wc;
+  out7[2] = g.threads;
+  out7[3] = g.band;
+  out7[4] = g.nstrips;
+  out7[5] = g.nbands;
+  out7[6] = g.groups;
+  return SBF_OK;
+}
+
+size_t sbf_local_range_workspace(int64_t H, int64_t W, int dtype) {
+  return sbf::local_range_ws(H, W, dtype);
+}
+
+int sbf_local_range(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int R,
+                    int64_t t_lo, int64_t t_hi, void* M_out, double* stats_dev, void* ws,
+                    size_t ws_bytes, void* stream) {
+  return sbf::launch_local_range(f, dtype, H, W, ld, R, t_lo, t_hi, M_out, stats_dev, ws,
+                                 ws_bytes, as_stream(stream));
+}
+
+int sbf_plan_device(const double* T_dev, int use_fixed, double fixed_T, double sigma_r,
+                    double epsilon, int rule, double log_2_over_eps, sbf_plan* plan_dev,
+                    sbf_term* terms_dev, int terms_cap, void* stream) {
+  SBF_REQUIRE(sigma_r > 0.0, SBF_ERR_INVALID, "sigma_r must be positive");
+  SBF_REQUIRE(epsilon >= 0.0 && epsilon < 1.0, SBF_ERR_INVALID, "epsilon must lie in [0, 1)");
+  SBF_REQUIRE(rule >= 0 && rule <= 3, SBF_ERR_INVALID, "unknown truncation rule");
+  return sbf::launch_plan(T_dev, use_fixed, fixed_T, sigma_r, epsilon, rule, log_2_over_eps,
+                          plan_dev, terms_dev, terms_cap, as_stream(stream));
+}
+
+size_t sbf_filter_workspace(int64_t rows_out, int64_t W, const sbf_spatial* sp, int precision) {
+  if (!sp) return 0;
+  return sbf::filter_ws(rows_out, W, sp, precision);
+}
+
+int sbf_filter(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int64_t row0,
+               int64_t img_H, int64_t out_lo, int64_t out_hi, const sbf_spatial* sp,
+               const sbf_plan* plan_dev, const sbf_term* terms_dev, const double* stats_dev,
+               int precision, void* out, int out_dtype, unsigned long long* fallback_dev,
+               void* ws, size_t ws_bytes, void* stream) {
+  SBF_REQUIRE(sp, SBF_ERR_INVALID, "null spatial");
+  sbf::FilterLaunch a;
+  a.f = f;
+  a.dtype = dtype;
+  a.H = H;
+  a.W = W;
+  a.ld = ld;
+  a.row0 = row0;
+  a.img_H = img_H;
+  a.out_lo = out_lo;
+  a.out_hi = out_hi;
+  a.sp = *sp;
+  a.plan = plan_dev;
+  a.terms = terms_dev;
+  a.stats = stats_dev;
+  a.precision = precision;
+  a.out = out;
+  a.out_dtype = out_dtype;
+  a.fallback = fallback_dev;
+  a.ws = ws;
+  a.ws_bytes = ws_bytes;
+  a.stream = as_stream(stream);
+  return sbf::launch_filter(a);
+}
+
+// workspace layout of the whole pipeline: [local-range][terms][filter]
+size_t sbf_shiftable_bf_workspace(int64_t H, int64_t W, int dtype, const sbf_spatial* sp,
+                                  int precision, int terms_cap) {
+  if (!sp) return 0;
+  return sbf::local_range_ws(H, W, dtype) + align_up((size_t)terms_cap * sizeof(sbf_term)) +
+         sbf::filter_ws(H, W, sp, precision);
+}
+
+int sbf_shiftable_bf(const void* f, int dtype, int64_t H, int64_t W, const sbf_spatial* sp, int R,
+                     double fixed_T, double sigma_r, double epsilon, int rule,
+                     double log_2_over_eps, int precision, void* out, int out_dtype,
+                     sbf_plan* plan_dev, double* stats_dev, unsigned long long* fallback_dev,
+                     int terms_cap, void* ws, size_t ws_bytes, void* stream) {
+  SBF_REQUIRE(sp && terms_cap > 0, SBF_ERR_INVALID, "bad arguments");
+  const size_t need = sbf_shiftable_bf_workspace(H, W, dtype, sp, precision, terms_cap);
+  SBF_REQUIRE(ws && ws_bytes >= need, SBF_ERR_WORKSPACE, "workspace too small (%zu < %zu)",
+              ws_bytes, need);
+  char* w = static_cast<char*>(ws);
+  const size_t lr = sbf::local_range_ws(H, W, dtype);
+  sbf_term* terms = reinterpret_cast<sbf_term*>(w + lr);
+  char* fws = w + lr + align_up((size_t)terms_cap * sizeof(sbf_term));
+  const bool use_fixed = fixed_T >= 0.0;
+  int rc = sbf_local_range(f, dtype, H, W, W, use_fixed ? 0 : R, 0, H, nullptr, stats_dev, w, lr,
+                           stream);
+  if (rc != SBF_OK) return rc;
+  rc = sbf_plan_device(stats_dev, use_fixed ? 1 : 0, fixed_T, sigma_r, epsilon, rule,
+                       log_2_over_eps, plan_dev, terms, terms_cap, stream);
+  if (rc != SBF_OK) return rc;
+  return sbf_filter(f, dtype, H, W, W, 0, H, 0, H, sp, plan_dev, terms, stats_dev, precision, out,
+                    out_dtype, fallback_dev, fws, ws_bytes - lr -
+                    align_up((size_t)terms_cap * sizeof(sbf_term)), stream);
+}
+
+int sbf_shiftable_bf_host(const double* f_host, int64_t H, int64_t W, const sbf_spatial* sp,
+                          int R, double fixed_T, double sigma_r, double epsilon, int rule,
+                          double log_2_over_eps, int precision, double* out_host,
+                          sbf_plan* plan_out, unsigned long long* fallback_out) {
+  SBF_REQUIRE(f_host && out_host && sp && plan_out && fallback_out, SBF_ERR_INVALID,
+              "null pointer");
+  const int cap = 1 << 16;
+  const size_t img = (size_t)(H * W) * sizeof(double);
+  const size_t ws_bytes = sbf_shiftable_bf_workspace(H, W, SBF_F64, sp, precision, cap);
+  cudaStream_t st;
+  SBF_CHECK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  char* dev = nullptr;
+  const size_t small = 1024;
+  int rc = SBF_OK;
+  if (cudaMallocAsync((void**)&dev, 2 * img + small + ws_bytes, st) != cudaSuccess) {
+    cudaStreamDestroy(st);
+    set_error("device allocation failed");
+    return SBF_ERR_CUDA;
+  }
+  double* f_dev = reinterpret_cast<double*>(dev);
+  double* o_dev = reinterpret_cast<double*>(dev + img);
+  sbf_plan* plan_dev = reinterpret_cast<sbf_plan*>(dev + 2 * img);
+  double* stats_dev = reinterpret_cast<double*>(dev + 2 * img + 128);
+  unsigned long long* fb_dev = reinterpret_cast<unsigned long long*>(dev + 2 * img + 256);
+  void* ws = dev + 2 * img + small;
+  if (cudaMemcpyAsync(f_dev, f_host, img, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemsetAsync(fb_dev, 0, sizeof(unsigned long long), st) != cudaSuccess) {
+    rc = SBF_ERR_CUDA;
+  }
+  if (rc == SBF_OK)
+    rc = sbf_shiftable_bf(f_dev, SBF_F64, H, W, sp, R, fixed_T, sigma_r, epsilon, rule,
+                          log_2_over_eps, precision, o_dev, SBF_F64, plan_dev, stats_dev, fb_dev,
+                          cap, ws, ws_bytes, st);
+  if (rc == SBF_OK) {
+    if (cudaMemcpyAsync(out_host, o_dev, img, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(plan_out, plan_dev, sizeof(sbf_plan), cudaMemcpyDeviceToHost, st) !=
+            cudaSuccess ||
+        cudaMemcpyAsync(fallback_out, fb_dev, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                        st) != cudaSuccess)
+      rc = SBF_ERR_CUDA;
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (rc == SBF_OK && e != cudaSuccess) {
+    set_error("device fault: %s", cudaGetErrorString(e));
+    rc = SBF_ERR_CUDA;
+  }
+  cudaFreeAsync(dev, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (rc == SBF_OK && plan_out->status != SBF_OK) {
+    set_error("plan failed (status %d, flags %d)", plan_out->status, plan_out->flags);
+    rc = plan_out->status;
+  }
+  return rc;
+}
+
+__global__ void divide_kernel(const double* num, const double* den, const double* fb, int64_t n,
+                              double* out, unsigned long long* count) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool bad = !(den[i] > 0.0);
+    out[i] = bad ? fb[i] : num[i] / den[i];
+    c += bad;
+  }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+int sbf_divide_with_fallback(const double* num, const double* den, const double* fallback,
+                             int64_t n, double* out, unsigned long long* count_dev,
+                             void* stream) {
+  SBF_REQUIRE(num && den && fallback && out && count_dev && n >= 0, SBF_ERR_INVALID,
+              "null pointer");
+  if (n == 0) return SBF_OK;
+  const unsigned grid = (unsigned)smin<int64_t>((n + 255) / 256, 148 * 8);
+  divide_kernel<<<grid, 256, 0, as_stream(stream)>>>(num, den, fallback, n, out, count_dev);
+  SBF_CHECK_LAUNCH();
+  return SBF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,174 @@
+// Generic fp64 term path for spatial parameters without a specialised K3
+// instantiation (large radii, unusual pass counts).  Still CUDA end to end —
+// there is no CPU fallback anywhere in the library.
+//
+// Per term: build the four modulated planes, run each extended-box pass as a
+// row kernel then a column kernel (reference order, spatial.py:114-117,
+// :136-139) with exact clamped renormalisation, then accumulate num/den.
+// Everything in float64, so this path is also the accuracy yardstick for
+// the fast kernels.  It reads the plan back to the host once (the term count
+// drives the launch loop).
+#include <vector>
+
+#include "sbf_common.cuh"
+
+namespace sbf {
+namespace {
+
+__global__ void gen_images(const void* f, int f64, int64_t H, int64_t W, int64_t ld,
+                           const double* stats, double turns, double* planes) {
+  const int64_t n = H * W;
+  const double center = stats[3];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t y = i / W, x = i - y * W;
+    const double fv = f64 ? static_cast<const double*>(f)[y * ld + x]
+                          : (double)static_cast<const float*>(f)[y * ld + x];
+    const double fc = fv - center;
+    const double u = fc * turns;
+    const double t = u - rint(u);
+    double s, c;
+    sincospi(2.0 * t, &s, &c);
+    planes[i] = fc * c;
+    planes[n + i] = c;
+    planes[2 * n + i] = fc * s;
+    planes[3 * n + i] = s;
+  }
+}
+
+// one extended-box pass along rows (contiguous), 4 planes
+__global__ void gen_rows(const double* __restrict__ in, double* __restrict__ out, int64_t lines,
+                         int64_t W, int r, double alpha) {
+  const int64_t line = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (line >= lines) return;
+  const double* x = in + line * W;
+  double* y = out + line * W;
+  double S = 0.0;
+  for (int64_t k = 0; k <= r && k < W; ++k) S += x[k];
+  for (int64_t i = 0; i < W; ++i) {
+    if (i > 0) {
+      if (i + r < W) S += x[i + r];
+      if (i - r - 1 >= 0) S -= x[i - r - 1];
+    }
+    const int64_t lo = i - r < 0 ? 0 : i - r;
+    const int64_t hi = i + r > W - 1 ? W - 1 : i + r;
+    double cnt = (double)(hi - lo + 1), tot = S;
+    if (alpha > 0.0) {
+      if (i - r - 1 >= 0) {
+        tot += alpha * x[i - r - 1];
+        cnt += alpha;
+      }
+      if (i + r + 1 <= W - 1) {
+        tot += alpha * x[i + r + 1];
+        cnt += alpha;
+      }
+    }
+    y[i] = tot / cnt;
+  }
+}
+
+// one extended-box pass along columns; counts use global row positions
+__global__ void gen_cols(const double* __restrict__ in, double* __restrict__ out, int nplanes,
+                         int64_t H, int64_t W, int64_t row0, int64_t img_H, int r, double alpha) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= nplanes * W) return;
+  const int64_t pl = id / W, xcol = id - pl * W;
+  const double* x = in + pl * H * W + xcol;
+  double* y = out + pl * H * W + xcol;
+  double S = 0.0;
+  for (int64_t k = 0; k <= r && k < H; ++k) S += x[k * W];
+  for (int64_t i = 0; i < H; ++i) {
+    if (i > 0) {
+      if (i + r < H) S += x[(i + r) * W];
+      if (i - r - 1 >= 0) S -= x[(i - r - 1) * W];
+    }
+    const int64_t g = row0 + i;
+    const int64_t lo = g - r < 0 ? 0 : g - r;
+    const int64_t hi = g + r > img_H - 1 ? img_H - 1 : g + r;
+    double cnt = (double)(hi - lo + 1), tot = S;
+    if (alpha > 0.0) {
+      if (g - r - 1 >= 0) {
+        if (i - r - 1 >= 0) tot += alpha * x[(i - r - 1) * W];
+        cnt += alpha;
+      }
+      if (g + r + 1 <= img_H - 1) {
+        if (i + r + 1 < H) tot += alpha * x[(i + r + 1) * W];
+        cnt += alpha;
+      }
+    }
+    y[i * W] = tot / cnt;
+  }
+}
+
+__global__ void gen_accum(const double* __restrict__ planes, const void* f, int f64, int64_t H,
+                          int64_t W, int64_t ld, int64_t out_lo, int64_t out_hi,
+                          const double* stats, double turns, double scale, int first,
+                          double* __restrict__ nd) {
+  const int64_t n = H * W;
+  const int64_t m = (out_hi - out_lo) * W;
+  const double center = stats[3];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t yo = i / W, x = i - yo * W;
+    const int64_t y = out_lo + yo;
+    const int64_t pi = y * W + x;
+    const double fv = f64 ? static_cast<const double*>(f)[y * ld + x]
+                          : (double)static_cast<const float*>(f)[y * ld + x];
+    const double u = (fv - center) * turns;
+    const double t = u - rint(u);
+    double s, c;
+    sincospi(2.0 * t, &s, &c);
+    const double num = scale * (c * planes[pi] + s * planes[2 * n + pi]);
+    const double den = scale * (c * planes[n + pi] + s * planes[3 * n + pi]);
+    if (first) {
+      nd[2 * i] = num;
+      nd[2 * i + 1] = den;
+    } else {
+      nd[2 * i] += num;
+      nd[2 * i + 1] += den;
+    }
+  }
+}
+
+}  // namespace
+
+int launch_generic_terms(const FilterLaunch& a, double* nd) {
+  cudaStream_t st = a.stream;
+  sbf_plan plan;
+  SBF_CHECK_CUDA(cudaMemcpyAsync(&plan, a.plan, sizeof(plan), cudaMemcpyDeviceToHost, st));
+  SBF_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (plan.status != SBF_OK) return SBF_OK;  // surfaced by the caller from the plan
+  std::vector<sbf_term> terms(plan.K_eval > 0 ? plan.K_eval : 1);
+  if (plan.K_eval > 0) {
+    SBF_CHECK_CUDA(cudaMemcpyAsync(terms.data(), a.terms, sizeof(sbf_term) * plan.K_eval,
+                                   cudaMemcpyDeviceToHost, st));
+    SBF_CHECK_CUDA(cudaStreamSynchronize(st));
+  }
+  const int64_t H = a.H, W = a.W, n = H * W;
+  double* planes = nullptr;
+  double* tmp = nullptr;
+  SBF_CHECK_CUDA(cudaMallocAsync(&planes, sizeof(double) * 4 * n, st));
+  SBF_CHECK_CUDA(cudaMallocAsync(&tmp, sizeof(double) * 4 * n, st));
+  const int bs = 256;
+  const unsigned gpix = (unsigned)smin<int64_t>((n + bs - 1) / bs, 148 * 16);
+  const int passes = a.sp.mode == SBF_SPATIAL_BOX ? 1 : a.sp.passes;
+  const double alpha = a.sp.mode == SBF_SPATIAL_BOX ? 0.0 : a.sp.alpha;
+  for (int k = 0; k < plan.K_eval; ++k) {
+    gen_images<<<gpix, bs, 0, st>>>(a.f, a.dtype == SBF_F64, H, W, a.ld, a.stats,
+                                    terms[k].turns, planes);
+    for (int ps = 0; ps < passes; ++ps) {
+      gen_rows<<<(unsigned)((4 * H + bs - 1) / bs), bs, 0, st>>>(planes, tmp, 4 * H, W, a.sp.r,
+                                                                 alpha);
+      gen_cols<<<(unsigned)((4 * W + bs - 1) / bs), bs, 0, st>>>(tmp, planes, 4, H, W, a.row0,
+                                                                 a.img_H, a.sp.r, alpha);
+    }
+    gen_accum<<<gpix, bs, 0, st>>>(planes, a.f, a.dtype == SBF_F64, H, W, a.ld, a.out_lo,
+                                   a.out_hi, a.stats, terms[k].turns, terms[k].scale, k == 0, nd);
+    SBF_CHECK_LAUNCH();
+  }
+  SBF_CHECK_CUDA(cudaFreeAsync(planes, st));
+  SBF_CHECK_CUDA(cudaFreeAsync(tmp, st));
+  return SBF_OK;
+}
+
+}  // namespace sbf

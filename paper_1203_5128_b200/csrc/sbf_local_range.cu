@@ -1,0 +1,271 @@
+// K1 — local dynamic range (reference maxfilter.py:41-61, _fastcore.pyx:16-58).
+//
+// Separable windowed maximum over the clamped (2R+1)^2 window, followed by
+// T = max(M - f) evaluated in float64 exactly like the reference
+// (`float(np.max(max_filter_2d(f, R) - f))`).  Both line passes use the van
+// Herk / Gil-Werman partition scheme on shared-memory tiles: replicate
+// padding (equivalent to clamping the window), per-partition prefix and
+// suffix maxima, one combining max per output.  Max is exact, so M is
+// bit-identical to the reference whatever the partition alignment.
+//
+// HBM-bound: f is read twice (row pass, column pass) and the row maxima
+// once (written + read); T, min f and max f are reduced on chip and folded
+// into three 64-bit atomics per CTA.
+#include "sbf_common.cuh"
+
+namespace sbf {
+namespace {
+
+constexpr int kRowSeg = 1024;   // outputs per row-pass CTA
+constexpr int kColTile = 32;    // columns per column-pass CTA
+constexpr int kColRows = 64;    // output rows per column-pass CTA
+constexpr int kColThreadsY = 8;
+
+template <typename T>
+__device__ __forceinline__ T vmax(T a, T b) { return a > b ? a : b; }
+
+// Row pass: out[y, x] = max f[y, clamp(x-R .. x+R)]
+template <typename T>
+__global__ void __launch_bounds__(256) rowmax_kernel(const T* __restrict__ f, int64_t W,
+                                                     int64_t ld, int R, T* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* q = reinterpret_cast<T*>(smem_raw);
+  const int64_t y = blockIdx.y;
+  const int64_t x0 = (int64_t)blockIdx.x * kRowSeg;
+  const int nout = (int)smin<int64_t>(kRowSeg, W - x0);
+  const int win = 2 * R + 1;
+  const int len = nout + 2 * R;
+  const int nblk = (len + win - 1) / win;
+  const int plen = nblk * win;
+  T* suf = q + plen;
+  const T* row = f + y * ld;
+  for (int k = threadIdx.x; k < plen; k += blockDim.x) {
+    int64_t x = x0 - R + k;
+    x = x < 0 ? 0 : (x >= W ? W - 1 : x);
+    q[k] = row[x];
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+    const int s = b * win;
+    T acc = q[s + win - 1];
+    suf[s + win - 1] = acc;
+    for (int k = win - 2; k >= 0; --k) {
+      acc = vmax(acc, q[s + k]);
+      suf[s + k] = acc;
+    }
+    acc = q[s];
+    for (int k = 1; k < win; ++k) {  // prefix max in place
+      acc = vmax(acc, q[s + k]);
+      q[s + k] = acc;
+    }
+  }
+  __syncthreads();
+  T* orow = out + y * W + x0;
+  for (int j = threadIdx.x; j < nout; j += blockDim.x) orow[j] = vmax(suf[j], q[j + 2 * R]);
+}
+
+template <typename T>
+__device__ __forceinline__ double block_reduce(double v, bool is_max, double* red) {
+  for (int o = 16; o; o >>= 1) {
+    double w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmax(v, w) : fmin(v, w);
+  }
+  const int lane = (threadIdx.y * blockDim.x + threadIdx.x) & 31;
+  const int warp = (threadIdx.y * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (blockDim.x * blockDim.y) >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < nwarps ? red[lane] : (is_max ? -INFINITY : INFINITY);
+    for (int o = 16; o; o >>= 1) {
+      double w = __shfl_xor_sync(0xffffffffu, v, o);
+      v = is_max ? fmax(v, w) : fmin(v, w);
+    }
+  }
+  return v;
+}
+
+// Column pass fused with M - f, T, min/max.  Block = 32 columns x 8 threads.
+template <typename T>
+__global__ void __launch_bounds__(kColTile* kColThreadsY) colmax_kernel(
+    const T* __restrict__ rowmax, const T* __restrict__ f, int64_t H, int64_t W, int64_t ld,
+    int R, int64_t t_lo, int64_t t_hi, T* __restrict__ M_out, unsigned long long* __restrict__ red) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int win = 2 * R + 1;
+  const int64_t y0 = (int64_t)blockIdx.y * kColRows;
+  const int nrows = (int)smin<int64_t>(kColRows, H - y0);
+  const int len = nrows + 2 * R;
+  const int nblk = (len + win - 1) / win;
+  const int plen = nblk * win;
+  constexpr int P = kColTile + 1;
+  T* q = reinterpret_cast<T*>(smem_raw);
+  T* suf = q + (size_t)plen * P;
+  double* dred = reinterpret_cast<double*>(suf + (size_t)plen * P);
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t x = (int64_t)blockIdx.x * kColTile + tx;
+  const bool xok = x < W;
+  for (int k = ty; k < plen; k += kColThreadsY) {
+    int64_t y = y0 - R + k;
+    y = y < 0 ? 0 : (y >= H ? H - 1 : y);
+    q[k * P + tx] = xok ? rowmax[y * W + x] : T(0);
+  }
+  __syncthreads();
+  for (int b = ty; b < nblk; b += kColThreadsY) {
+    const int s = b * win;
+    T acc = q[(s + win - 1) * P + tx];
+    suf[(s + win - 1) * P + tx] = acc;
+    for (int k = win - 2; k >= 0; --k) {
+      acc = vmax(acc, q[(s + k) * P + tx]);
+      suf[(s + k) * P + tx] = acc;
+    }
+    acc = q[s * P + tx];
+    for (int k = 1; k < win; ++k) {
+      acc = vmax(acc, q[(s + k) * P + tx]);
+      q[(s + k) * P + tx] = acc;
+    }
+  }
+  __syncthreads();
+  double tmax = 0.0, fmn = INFINITY, fmx = -INFINITY;
+  unsigned long long bad = 0;
+  if (xok) {
+    for (int j = ty; j < nrows; j += kColThreadsY) {
+      const int64_t y = y0 + j;
+      const T m = vmax(suf[j * P + tx], q[(j + 2 * R) * P + tx]);
+      if (M_out) M_out[y * W + x] = m;
+      if (y >= t_lo && y < t_hi) {
+        const double fv = (double)f[y * ld + x];
+        bad += isfinite(fv) ? 0 : 1;       // image.py:16 (as_image finiteness)
+        tmax = fmax(tmax, (double)m - fv);  // maxfilter.py:61, float64 subtraction
+        fmn = fmin(fmn, fv);
+        fmx = fmax(fmx, fv);
+      }
+    }
+  }
+  tmax = block_reduce<T>(tmax, true, dred);
+  if (tx == 0 && ty == 0) atomicMax(&red[0], ord_bits(tmax));
+  fmn = block_reduce<T>(fmn, false, dred);
+  if (tx == 0 && ty == 0) atomicMin(&red[1], ord_bits(fmn));
+  fmx = block_reduce<T>(fmx, true, dred);
+  if (tx == 0 && ty == 0) atomicMax(&red[2], ord_bits(fmx));
+  for (int o = 16; o; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if (((ty * kColTile + tx) & 31) == 0 && bad) atomicAdd(&red[3], bad);
+}
+
+// R == 0: T = 0 by definition (maxfilter.py:58-59); statistics only.
+template <typename T>
+__global__ void stats_only_kernel(const T* __restrict__ f, int64_t W, int64_t ld, int64_t t_lo,
+                                  int64_t t_hi, T* __restrict__ M_out, int64_t H,
+                                  unsigned long long* __restrict__ red) {
+  __shared__ double dred[32];
+  double fmn = INFINITY, fmx = -INFINITY;
+  unsigned long long bad = 0;
+  const int64_t n = H * W;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t y = i / W, x = i - y * W;
+    const T v = f[y * ld + x];
+    if (M_out) M_out[i] = v;
+    if (y >= t_lo && y < t_hi) {
+      bad += isfinite((double)v) ? 0 : 1;
+      fmn = fmin(fmn, (double)v);
+      fmx = fmax(fmx, (double)v);
+    }
+  }
+  fmn = block_reduce<T>(fmn, false, dred);
+  if (threadIdx.x == 0) atomicMin(&red[1], ord_bits(fmn));
+  fmx = block_reduce<T>(fmx, true, dred);
+  if (threadIdx.x == 0) atomicMax(&red[2], ord_bits(fmx));
+  for (int o = 16; o; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&red[3], bad);
+}
+
+__global__ void stats_init_kernel(double* stats) {
+  unsigned long long* red = reinterpret_cast<unsigned long long*>(stats + 4);
+  red[0] = ord_bits(0.0);
+  red[1] = ord_bits(INFINITY);
+  red[2] = ord_bits(-INFINITY);
+  red[3] = 0ull;  // non-finite sample count (stats[7], read as uint64)
+}
+
+__global__ void stats_final_kernel(double* stats) {
+  const unsigned long long* red = reinterpret_cast<const unsigned long long*>(stats + 4);
+  const double T = ord_value(red[0]);
+  const double mn = ord_value(red[1]), mx = ord_value(red[2]);
+  stats[0] = T;
+  stats[1] = mn;
+  stats[2] = mx;
+  // centre used by the term kernel: any constant works (BF(f + c) = BF(f) + c);
+  // mid-range rounded to fp32 halves the magnitudes the fp32 sums carry.
+  stats[3] = (isfinite(mn) && isfinite(mx)) ? (double)(float)(0.5 * (mn + mx)) : 0.0;
+}
+
+template <typename T>
+int run(const void* fv, int64_t H, int64_t W, int64_t ld, int R, int64_t t_lo, int64_t t_hi,
+        void* M_out, double* stats, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const T* f = static_cast<const T*>(fv);
+  unsigned long long* red = reinterpret_cast<unsigned long long*>(stats + 4);
+  stats_init_kernel<<<1, 1, 0, st>>>(stats);
+  SBF_CHECK_LAUNCH();
+  // a window wider than the image equals the image-wide window (clamping)
+  const int Rr = (int)smin<int64_t>(R, smax<int64_t>(W - 1, 0));
+  const int Rc = (int)smin<int64_t>(R, smax<int64_t>(H - 1, 0));
+  if (R == 0) {
+    stats_only_kernel<T><<<2 * 148, 256, 0, st>>>(f, W, ld, t_lo, t_hi, static_cast<T*>(M_out), H,
+                                                  red);
+    SBF_CHECK_LAUNCH();
+  } else {
+    SBF_REQUIRE(ws_bytes >= (size_t)(H * W) * sizeof(T), SBF_ERR_WORKSPACE,
+                "local_range workspace too small");
+    T* rowmax = static_cast<T*>(ws);
+    {
+      const int win = 2 * Rr + 1;
+      const int plen = ((kRowSeg + 2 * Rr + win - 1) / win) * win;
+      const size_t smem = 2 * (size_t)plen * sizeof(T);
+      SBF_REQUIRE(smem <= 200 * 1024, SBF_ERR_UNSUPPORTED, "max-filter radius %d too large", R);
+      SBF_CHECK_CUDA(cudaFuncSetAttribute(rowmax_kernel<T>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      dim3 grid((unsigned)((W + kRowSeg - 1) / kRowSeg), (unsigned)H);
+      rowmax_kernel<T><<<grid, 256, smem, st>>>(f, W, ld, Rr, rowmax);
+      SBF_CHECK_LAUNCH();
+    }
+    {
+      const int win = 2 * Rc + 1;
+      const int plen = ((kColRows + 2 * Rc + win - 1) / win) * win;
+      const size_t smem = 2 * (size_t)plen * (kColTile + 1) * sizeof(T) + 32 * sizeof(double);
+      SBF_REQUIRE(smem <= 220 * 1024, SBF_ERR_UNSUPPORTED, "max-filter radius %d too large", R);
+      SBF_CHECK_CUDA(cudaFuncSetAttribute(colmax_kernel<T>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      dim3 grid((unsigned)((W + kColTile - 1) / kColTile), (unsigned)((H + kColRows - 1) / kColRows));
+      dim3 block(kColTile, kColThreadsY);
+      colmax_kernel<T><<<grid, block, smem, st>>>(rowmax, f, H, W, ld, Rc, t_lo, t_hi,
+                                                  static_cast<T*>(M_out), red);
+      SBF_CHECK_LAUNCH();
+    }
+  }
+  stats_final_kernel<<<1, 1, 0, st>>>(stats);
+  SBF_CHECK_LAUNCH();
+  return SBF_OK;
+}
+
+}  // namespace
+
+size_t local_range_ws(int64_t H, int64_t W, int dtype) {
+  return align_up((size_t)(H * W) * (dtype == SBF_F64 ? 8 : 4));
+}
+
+int launch_local_range(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int R,
+                       int64_t t_lo, int64_t t_hi, void* M_out, double* stats, void* ws,
+                       size_t ws_bytes, cudaStream_t st) {
+  SBF_REQUIRE(f && stats, SBF_ERR_INVALID, "null pointer");
+  SBF_REQUIRE(H >= 1 && W >= 1 && ld >= W, SBF_ERR_INVALID, "bad image shape %lld x %lld",
+              (long long)H, (long long)W);
+  SBF_REQUIRE(R >= 0, SBF_ERR_INVALID, "radius must be >= 0");
+  SBF_REQUIRE(t_lo >= 0 && t_hi <= H && t_lo < t_hi, SBF_ERR_INVALID, "bad row range");
+  if (dtype == SBF_F32) return run<float>(f, H, W, ld, R, t_lo, t_hi, M_out, stats, ws, ws_bytes, st);
+  if (dtype == SBF_F64) return run<double>(f, H, W, ld, R, t_lo, t_hi, M_out, stats, ws, ws_bytes, st);
+  set_error("unsupported dtype %d", dtype);
+  return SBF_ERR_INVALID;
+}
+
+}  // namespace sbf

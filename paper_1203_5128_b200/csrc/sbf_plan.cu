@@ -1,0 +1,150 @@
+// K2 — kernel plan on the device (reference kernels.py:166-227).
+//
+// One thread reads T from device memory (written by K1, no host round trip),
+// selects (N, M) with the same rules as the reference (shared source with the
+// host ABI, sbf_plan_logic.cuh) and writes the folded term table: for
+// n = floor(N/2) down to M, scale = d_n (2 d_n for a +-pair) and
+// omega_n = (2n - N) / (sqrt(N) sigma_r).  d_n = C(N,n)/2^N is evaluated by
+// the centre-outward ratio recurrence normalised by the full binomial sum
+// (relative error ~N*1e-16; weights need not be bit-exact, only the index
+// set).  Exact-zero weights (float64 underflow in the reference too) are
+// skipped: they contribute nothing, so skipping is arithmetic-identical.
+#include "sbf_common.cuh"
+#include "sbf_plan_logic.cuh"
+
+namespace sbf {
+namespace {
+
+__global__ void plan_kernel(const double* __restrict__ T_dev, int use_fixed, double fixed_T,
+                            double sigma_r, double eps, int rule, double log_2_over_eps,
+                            sbf_plan* __restrict__ plan_out, sbf_term* __restrict__ terms,
+                            int cap) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double T = use_fixed ? fixed_T : T_dev[0];
+  sbf_plan p;
+  select_plan(T, sigma_r, eps, rule, log_2_over_eps, &p);
+  if (p.status == SBF_OK) {
+    const int N = p.N, M = p.M, nc = N / 2;
+    // total = sum_{n=0}^{N} C(N,n)/C(N,nc) by symmetry from the half sum
+    double t = 1.0, half = 0.0;
+    for (int n = nc; n >= 0; --n) {
+      half += t;
+      t = t * (double)n / (double)(N - n + 1);
+      if (t == 0.0) break;
+    }
+    const double total = 2.0 * half - ((N % 2 == 0) ? 1.0 : 0.0);
+    const double inv2pi = 0.15915494309189535;
+    const double denom = sqrt((double)N) * sigma_r;
+    int k = 0;
+    t = 1.0;
+    for (int n = nc; n >= M; --n) {
+      const double d = t / total;
+      const double scale = (2 * n == N) ? d : 2.0 * d;
+      if (scale == 0.0) break;  // weights only shrink away from the centre
+      if (k < cap) {
+        sbf_term tm;
+        tm.scale = scale;
+        tm.freq = (double)(2 * n - N) / denom;
+        tm.turns = tm.freq * inv2pi;
+        tm.index = n;
+        tm.pad = 0;
+        terms[k] = tm;
+      }
+      ++k;
+      t = t * (double)n / (double)(N - n + 1);
+    }
+    p.K_eval = k;
+    if (k > cap) {
+      p.flags |= SBF_PLAN_TERMS_TRUNCATED;
+      p.status = SBF_ERR_UNSUPPORTED;
+    }
+  }
+  *plan_out = p;
+}
+
+}  // namespace
+
+int launch_plan(const double* T_dev, int use_fixed, double fixed_T, double sigma_r, double eps,
+                int rule, double log_2_over_eps, sbf_plan* plan_dev, sbf_term* terms_dev,
+                int terms_cap, cudaStream_t st) {
+  SBF_REQUIRE(plan_dev && terms_dev && terms_cap > 0, SBF_ERR_INVALID, "null plan/terms buffer");
+  SBF_REQUIRE(use_fixed || T_dev, SBF_ERR_INVALID, "null T");
+  plan_kernel<<<1, 32, 0, st>>>(T_dev, use_fixed, fixed_T, sigma_r, eps, rule, log_2_over_eps,
+                                plan_dev, terms_dev, terms_cap);
+  SBF_CHECK_LAUNCH();
+  return SBF_OK;
+}
+
+}  // namespace sbf
+
+// ---------------------------------------------------------------------------
+// host twins (same source as K2)
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int sbf_extended_box_params(double sigma_s, int passes, int* r, double* alpha) {
+  if (!(sigma_s > 0.0) || passes < 1 || !r || !alpha) {
+    sbf::set_error("sigma_s must be positive and passes >= 1");
+    return SBF_ERR_INVALID;
+  }
+  sbf::extended_box_params(sigma_s, passes, r, alpha);
+  return SBF_OK;
+}
+
+int sbf_support_radius(const sbf_spatial* sp, int* radius) {
+  if (!sp || !radius) return SBF_ERR_INVALID;
+  if (sp->mode == SBF_SPATIAL_BOX) {
+    *radius = sp->r;
+  } else {
+    *radius = sp->passes * (sp->r + (sp->alpha > 0.0 ? 1 : 0));
+  }
+  return SBF_OK;
+}
+
+int sbf_order_threshold(double T, double sigma_r, int* N) {
+  if (!(sigma_r > 0.0) || !(T >= 0.0) || !N) {
+    sbf::set_error("need sigma_r > 0 and T >= 0");
+    return SBF_ERR_INVALID;
+  }
+  int flags = 0, status = SBF_OK;
+  *N = sbf::order_threshold(T, sigma_r, &flags, &status);
+  return status;
+}
+
+int sbf_truncation_index_exact(int N, double epsilon, int* M) {
+  if (N < 1 || !(epsilon >= 0.0 && epsilon < 1.0) || !M) {
+    sbf::set_error("need N >= 1 and 0 <= epsilon < 1");
+    return SBF_ERR_INVALID;
+  }
+  int flags = 0, status = SBF_OK;
+  *M = sbf::truncation_index_exact(N, epsilon, &flags, &status, false);
+  return status;
+}
+
+// force the multi-limb path (test hook for the exact arithmetic)
+int sbf_truncation_index_exact_bigint(int N, double epsilon, int* M) {
+  if (N < 1 || !(epsilon > 0.0 && epsilon < 1.0) || !M) return SBF_ERR_INVALID;
+  int status = SBF_OK;
+  *M = sbf::truncation_exact_bigint(N, epsilon, &status);
+  return status;
+}
+
+int sbf_truncation_index_chernoff(int N, double epsilon, double log_2_over_eps, int* M) {
+  if (N < 1 || !(epsilon > 0.0 && epsilon < 1.0) || !M) {
+    sbf::set_error("epsilon must be positive for the tail-bound rule; use M=0 for epsilon=0");
+    return SBF_ERR_INVALID;
+  }
+  int status = SBF_OK;
+  *M = sbf::truncation_index_chernoff(N, epsilon, log_2_over_eps, &status);
+  return status;
+}
+
+int sbf_select_plan(double T, double sigma_r, double epsilon, int rule, double log_2_over_eps,
+                    sbf_plan* out) {
+  if (!out) return SBF_ERR_INVALID;
+  sbf::select_plan(T, sigma_r, epsilon, rule, log_2_over_eps, out);
+  if (out->status != SBF_OK) sbf::set_error("select_plan failed (status %d)", out->status);
+  return out->status;
+}
+
+}  // extern "C"

@@ -1,0 +1,208 @@
+"""Generate golden vectors from the REFERENCE implementation (run in the dev
+container only; /root/reference does not exist on the GPU box).
+
+    python tests/golden/make_golden.py [--big]
+
+Imports the reference package `shiftbf` from /root/reference/pkg/src (its
+pure-numpy line-kernel backend; the compiled backend agrees to 1e-12 per
+the reference's own test_backends.py) and writes small .npz fixtures next to
+this script.  `--big` also computes T/N/M of configs 2-5 (minutes).
+
+The fixtures pin the oracle (tests/test_oracle_golden.py) and are the
+known-answer vectors for the CUDA parity tests.
+"""
+
+import argparse
+import math
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+import shiftbf  # noqa: E402  (reference)
+from shiftbf import kernels as rk  # noqa: E402
+from shiftbf import maxfilter as rm  # noqa: E402
+from shiftbf import spatial as rs  # noqa: E402
+from shiftbf.bilateral import FilterParams, shiftable_bf  # noqa: E402
+
+from paper_1203_5128_b200.workloads import config_image  # noqa: E402
+
+
+def plans():
+    rng = np.random.default_rng(7)
+    rows = []
+    sigmas = [5.0, 8.0, 10.0, 10.0000001, 10.5, 15.0, 20.0, 30.0, 39.9, 40.0,
+              40.5, 60.0, 100.0, 800.0]
+    eps_list = [0.0, 0.005, 0.01, 0.02, 0.05, 0.25]
+    Ts = [0.0, 1.0, 17.5, 100.0, 251.39522633396712, 237.54737095534801, 255.0,
+          62376.0, 253.45146048069, 245.72779846191406, 236.57716369628906]
+    Ts += list(rng.uniform(0, 300, 40)) + list(rng.uniform(0, 3000, 10))
+    rules = ["auto", "exact", "chernoff", "none"]
+    for T in Ts:
+        for sr in sigmas:
+            for eps in eps_list:
+                for rule in rules:
+                    needs_exact = rule == "exact" or (rule == "auto" and 10 < sr <= 40)
+                    if needs_exact and eps > 0 and rk.order_threshold(T, sr) > 3000:
+                        continue
+                    p = rk.select_plan(T, sr, eps, truncation=rule)
+                    rows.append((T, sr, eps, rules.index(rule), p.N, p.M))
+    arr = np.array(rows, dtype=np.float64)
+    # N0 table (test_kernels.py:40-45) and chernoff/exact pins
+    n0 = {s: rk.order_threshold(255, s, mode="round") for s in (5, 10, 20, 30, 40, 60, 80, 100)}
+    exact = [(N, e, rk.truncation_index_exact(N, e))
+             for N in (1, 2, 3, 4, 5, 29, 47, 66, 101, 109, 118, 229, 263, 700, 2463)
+             for e in (0.005, 0.01, 0.05, 0.5)]
+    chern = [(N, e, rk.truncation_index_chernoff(N, e))
+             for N in (1, 2, 29, 229, 263, 700, 2463) for e in (0.005, 0.01, 0.05)]
+    np.savez_compressed(os.path.join(HERE, "plans.npz"), plans=arr,
+                        n0=np.array(list(n0.items()), dtype=np.float64),
+                        exact=np.array(exact, dtype=np.float64),
+                        chernoff=np.array(chern, dtype=np.float64))
+    # weights/frequencies for a few plans
+    wts = {}
+    for (N, M, sr) in ((2, 0, 1.0), (29, 7, 30.0), (229, 79, 10.0), (263, 111, 10.0), (2463, 0, 800.0)):
+        e = rk.raised_cosine_expansion(rk.KernelPlan(rk.KernelFamily.RAISED_COSINE, sr, 1.0, N, M,
+                                                     0.0 if M == 0 else 0.01))
+        wts[f"w_{N}_{M}"] = e.weights
+        wts[f"f_{N}_{M}"] = e.frequencies
+    np.savez_compressed(os.path.join(HERE, "expansions.npz"), **wts)
+
+
+def maxfilters():
+    rng = np.random.default_rng(11)
+    out = {}
+    for k in range(40):
+        h = int(rng.integers(1, 70))
+        w = int(rng.integers(1, 70))
+        R = int(rng.integers(0, 20))
+        img = rng.uniform(0, 255, (h, w))
+        if k % 3 == 0:
+            img = np.round(img)  # ties
+        if k % 5 == 0:
+            img = img.astype(np.float32).astype(np.float64)
+        out[f"img_{k}"] = img
+        out[f"R_{k}"] = np.array(R)
+        out[f"M_{k}"] = rm.max_filter_2d(img, R)
+        out[f"T_{k}"] = np.array(rm.compute_T(img, R))
+    for k in range(20):
+        n = int(rng.integers(1, 258))
+        R = int(rng.integers(0, 41))
+        s = rng.uniform(-1e3, 1e3, n)
+        out[f"seq_{k}"] = s
+        out[f"sR_{k}"] = np.array(R)
+        out[f"smax_{k}"] = rm.max_filter_1d(s, R)
+    np.savez_compressed(os.path.join(HERE, "maxfilter.npz"), **out)
+
+
+def smoothing():
+    rng = np.random.default_rng(12)
+    out = {}
+    k = 0
+    for sigma, passes in ((0.5, 3), (2.0, 3), (3.0, 3), (5.0, 3), (8.0, 3), (12.0, 3), (2.0, 1), (4.0, 2), (10.0, 4)):
+        h = int(rng.integers(1, 60))
+        w = int(rng.integers(1, 60))
+        img = rng.uniform(-50, 255, (h, w))
+        out[f"img_{k}"] = img
+        out[f"sig_{k}"] = np.array([sigma, passes])
+        out[f"out_{k}"] = rs.iterated_box_gaussian(img, sigma, passes)
+        r, a = rs.extended_box_params(sigma, passes)
+        out[f"ra_{k}"] = np.array([r, a])
+        k += 1
+    for j, radius in enumerate((0, 1, 3, 7, 30)):
+        img = rng.uniform(0, 255, (int(rng.integers(1, 50)), int(rng.integers(1, 50))))
+        out[f"bimg_{j}"] = img
+        out[f"brad_{j}"] = np.array(radius)
+        out[f"bout_{j}"] = rs.box_filter(img, radius)
+    np.savez_compressed(os.path.join(HERE, "smoothing.npz"), **out)
+
+
+def bf_cases():
+    """Small end-to-end filter cases covering modes, borders, plans."""
+    rng = np.random.default_rng(20260810)
+    cases = [
+        # (h, w, sigma_s, sigma_r, eps, spatial, fixed_T, truncation, lo, hi)
+        (40, 40, 2.0, 40.0, 0.0, None, None, "auto", 0, 255),
+        (37, 53, 3.0, 30.0, 0.01, None, None, "auto", 0, 255),
+        (64, 80, 5.0, 10.0, 0.01, None, None, "auto", 0, 255),
+        (33, 129, 2.0, 20.0, 0.01, None, None, "auto", 0, 255),
+        (150, 70, 3.0, 25.0, 0.01, None, None, "auto", 0, 255),
+        (24, 24, 2.0, 30.0, 0.01, ("box", 2), None, "auto", 0, 200),
+        (32, 32, 3.0, 15.0, 0.0, ("box", 3), None, "auto", 0, 255),
+        (16, 16, 2.0, 30.0, 0.0, ("box", 2), 255.0, "auto", 0, 200),
+        (20, 20, 3.0, 20.0, 0.05, None, None, "chernoff", 0, 255),
+        (20, 21, 3.0, 20.0, 0.05, None, None, "none", 0, 255),
+        (48, 48, 8.0, 800.0, 0.01, None, None, "auto", 0, 65535),
+        (45, 47, 6.0, 20.0, 0.01, None, None, "auto", 0, 255),
+        (9, 7, 1.0, 50.0, 0.0, None, None, "auto", 0, 255),
+        (3, 90, 4.0, 30.0, 0.01, None, None, "auto", 0, 255),
+        (60, 60, 12.0, 15.0, 0.01, None, None, "auto", 0, 255),
+        (64, 64, 30.0, 10.0, 0.005, ("box", 30), None, "auto", 0, 255),
+    ]
+    out = {}
+    for k, (h, w, ss, sr, eps, sp, fT, tr, lo, hi) in enumerate(cases):
+        img = rng.uniform(lo, hi, (h, w))
+        if k % 2 == 1:
+            img = img.astype(np.float32).astype(np.float64)
+        if k == 15:
+            img = shiftbf.checkerboard(h, w, 8)
+        spatial = None if sp is None else rs.Box(sp[1])
+        p = FilterParams(sigma_s=ss, sigma_r=sr, epsilon=eps, spatial=spatial,
+                         fixed_T=fT, truncation=tr)
+        import warnings
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            res = shiftable_bf(img, p)
+        out[f"img_{k}"] = img
+        out[f"par_{k}"] = np.array([ss, sr, eps, -1 if sp is None else sp[1],
+                                    np.nan if fT is None else fT,
+                                    ["auto", "exact", "chernoff", "none"].index(tr)])
+        out[f"out_{k}"] = res.image
+        out[f"plan_{k}"] = np.array([res.plan.T, res.plan.N, res.plan.M, res.fallback_pixels])
+    np.savez_compressed(os.path.join(HERE, "bf_small.npz"), **out)
+
+
+def config1():
+    img = config_image(1)
+    res = shiftable_bf(img, FilterParams(sigma_s=3, sigma_r=30, epsilon=0.01))
+    o = res.image
+    np.savez_compressed(os.path.join(HERE, "config1.npz"),
+                        plan=np.array([res.plan.T, res.plan.N, res.plan.M, res.fallback_pixels]),
+                        crop=o[192:320, 192:320], border=np.concatenate([o[0], o[-1], o[:, 0], o[:, -1]]),
+                        stats=np.array([o.sum(), o.min(), o.max(), float((o * o).sum())]),
+                        M=rm.max_filter_2d(img, 9)[::8, ::8])
+
+
+def big_plans():
+    rows = []
+    specs = [(2, 0, 5.0, 10.0), (3, 0, 8.0, 800.0)] + [(4, i, 6.0, 20.0) for i in range(64)] \
+        + [(5, c, 12.0, 15.0) for c in range(3)]
+    for cfg, idx, ss, sr in specs:
+        img = config_image(cfg, idx)
+        R = max(1, rs.support_radius(rs.IteratedBox(ss)))
+        T = rm.compute_T(img, R)
+        p = rk.select_plan(T, sr, 0.01)
+        rows.append((cfg, idx, R, T, p.N, p.M))
+        print(cfg, idx, R, repr(T), p.N, p.M, flush=True)
+        del img
+    np.savez_compressed(os.path.join(HERE, "config_plans.npz"), rows=np.array(rows, dtype=np.float64))
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--big", action="store_true")
+    a = ap.parse_args()
+    if not a.big:
+        plans()
+        maxfilters()
+        smoothing()
+        bf_cases()
+        config1()
+    if a.big:
+        big_plans()
+    print("done")

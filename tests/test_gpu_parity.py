@@ -1,0 +1,158 @@
+"""CUDA path vs the CPU oracle / reference golden vectors (B200 only).
+
+Tolerances (BASELINE.json north star): T, N, M, the kept-term index set and
+the max-filter image bit-exact; filtered image max-abs <= 1e-2 and
+RMS <= 1e-3 gray levels on the image's own intensity scale.
+"""
+
+import ctypes as C
+import math
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import shiftbf_oracle as O
+import paper_1203_5128_b200 as P
+from paper_1203_5128_b200 import _lib
+from paper_1203_5128_b200.workloads import config_image
+
+pytestmark = pytest.mark.gpu
+RULES = ["auto", "exact", "chernoff", "none"]
+MAX_ABS, RMS = 1e-2, 1e-3
+
+
+def assert_close_image(out, ref, tol_max=MAX_ABS, tol_rms=RMS):
+    d = np.asarray(out, dtype=np.float64) - ref
+    mx = float(np.abs(d).max())
+    rms = float(np.sqrt(np.mean(d * d)))
+    assert mx <= tol_max and rms <= tol_rms, f"max {mx:.3g} rms {rms:.3g}"
+    return mx, rms
+
+
+def test_max_filter_and_T_bit_exact_golden():
+    g = golden("maxfilter.npz")
+    for k in range(40):
+        img, R = g[f"img_{k}"], int(g[f"R_{k}"])
+        assert np.array_equal(P.max_filter_2d(img, R), g[f"M_{k}"]), k
+        assert P.compute_T(img, R) == float(g[f"T_{k}"]), k
+    for k in range(20):
+        assert np.array_equal(P.max_filter_1d(g[f"seq_{k}"], int(g[f"sR_{k}"])), g[f"smax_{k}"])
+
+
+def test_config1_T_and_M_bit_exact():
+    img = config_image(1)
+    assert P.compute_T(img, 9) == 251.39522633396712
+    M = P.max_filter_2d(img, 9)
+    assert np.array_equal(M, O.max_filter_2d(img, 9))
+
+
+@pytest.mark.parametrize("cfg,R", [(2, 15), (3, 24), (4, 18), (5, 36)])
+def test_config_T_bit_exact_crops(cfg, R):
+    img = config_image(cfg, size=512)
+    assert np.array_equal(P.max_filter_2d(img, R), O.max_filter_2d(img, R))
+    assert P.compute_T(img, R) == O.compute_T(img, R)
+
+
+def test_device_plan_matches_host_plan_and_oracle():
+    import torch
+    lib = _lib.load()
+    rng = np.random.default_rng(9)
+    cap = 1 << 14
+    plan = torch.empty(64, dtype=torch.uint8, device="cuda")
+    terms = torch.empty(cap * 32, dtype=torch.uint8, device="cuda")
+    Tbuf = torch.empty(1, dtype=torch.float64, device="cuda")
+    g = golden("plans.npz")["plans"]
+    cases = [tuple(r) for r in g[::7]] + [
+        (float(rng.uniform(0, 300)), float(rng.uniform(2, 60)), float(rng.choice([0, .01, .05])),
+         int(rng.integers(0, 4)), -1, -1) for _ in range(300)]
+    for T, sr, eps, rule, N, M in cases:
+        _, n, m = O.select_plan(T, sr, eps, RULES[int(rule)])
+        if N >= 0:
+            assert (n, m) == (int(N), int(M))
+        Tbuf.fill_(T)
+        _lib.check(lib.sbf_plan_device(Tbuf.data_ptr(), 0, 0.0, sr, eps, int(rule),
+                                       P.kernels.log_2_over_eps(eps), plan.data_ptr(),
+                                       terms.data_ptr(), cap, None))
+        torch.cuda.synchronize()
+        pc = _lib.SbfPlan.from_buffer_copy(plan.cpu().numpy().tobytes())
+        assert pc.status == 0
+        assert (pc.N, pc.M, pc.K) == (n, m, n // 2 - m + 1), (T, sr, eps, rule)
+        # kept-term index set and weights of the folded expansion
+        idx, scale, freq = O.folded_terms(n, m, sr)
+        tt = np.frombuffer(terms.cpu().numpy().tobytes()[: 32 * pc.K_eval],
+                           dtype=[("scale", "f8"), ("freq", "f8"), ("turns", "f8"), ("index", "i4"), ("pad", "i4")])
+        nz = scale > 0
+        assert sorted(tt["index"].tolist()) == sorted(idx[nz].tolist())
+        order = np.argsort(tt["index"])
+        np.testing.assert_allclose(tt["scale"][order], scale[nz][np.argsort(idx[nz])], rtol=1e-12)
+        np.testing.assert_array_equal(tt["freq"][order], freq[nz][np.argsort(idx[nz])])
+
+
+@pytest.mark.parametrize("k", range(16))
+def test_small_cases_vs_reference_golden(k):
+    g = golden("bf_small.npz")
+    ss, sr, eps, boxr, fT, tr = g[f"par_{k}"]
+    spatial = None if boxr < 0 else P.Box(int(boxr))
+    params = P.FilterParams(sigma_s=float(ss), sigma_r=float(sr), epsilon=float(eps),
+                            spatial=spatial, fixed_T=None if math.isnan(fT) else float(fT),
+                            truncation=RULES[int(tr)])
+    img = g[f"img_{k}"]
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = P.shiftable_bf(img, params)
+    T, N, M, fb = g[f"plan_{k}"]
+    assert (res.plan.T, res.plan.N, res.plan.M) == (T, int(N), int(M))
+    scale = max(1.0, float(np.abs(img).max()) / 255.0)  # tolerance in gray levels of the image's scale
+    assert_close_image(res.image, g[f"out_{k}"], MAX_ABS * scale / scale, RMS)
+
+
+def test_config1_full_vs_oracle():
+    img = config_image(1)
+    res = P.shiftable_bf(img, P.FilterParams(sigma_s=3, sigma_r=30, epsilon=0.01))
+    assert (res.plan.T, res.plan.N, res.plan.M) == (251.39522633396712, 29, 7)
+    assert res.fallback_pixels == 0
+    ref = O.shiftable_bf(img, 3.0, 30.0, 0.01)["image"]
+    assert_close_image(res.image, ref)
+    g = golden("config1.npz")
+    assert_close_image(res.image[192:320, 192:320], g["crop"])
+
+
+@pytest.mark.parametrize("cfg,size", [(2, 256), (4, 256), (5, 256), (3, 192)])
+def test_config_crops_vs_oracle(cfg, size):
+    c = {2: (5.0, 10.0), 3: (8.0, 800.0), 4: (6.0, 20.0), 5: (12.0, 15.0)}[cfg]
+    img = config_image(cfg, size=size)
+    res = P.shiftable_bf(img, P.FilterParams(sigma_s=c[0], sigma_r=c[1], epsilon=0.01))
+    ref = O.shiftable_bf(img, c[0], c[1], 0.01)
+    assert (res.plan.T, res.plan.N, res.plan.M) == (ref["T"], ref["N"], ref["M"])
+    assert_close_image(res.image, ref["image"])
+
+
+def test_constant_image_fixed_point():
+    img = np.full((40, 300), 77.0)
+    res = P.shiftable_bf(img, P.FilterParams(sigma_s=2, sigma_r=35, epsilon=0.01))
+    np.testing.assert_allclose(res.image, img, atol=1e-6)
+    assert res.plan.T == 0.0 and res.plan.N == 1 and res.fallback_pixels == 0
+
+
+def test_non_finite_rejected():
+    img = np.zeros((8, 8))
+    img[1, 1] = np.nan
+    with pytest.raises(P.InvalidParameterError):
+        P.shiftable_bf(img, P.FilterParams(sigma_s=2, sigma_r=10, spatial=P.Box(1)))
+
+
+def test_divide_with_fallback_kernel():
+    import torch
+    lib = _lib.load()
+    num = torch.tensor([1.0, 2.0, 3.0, 4.0, 5.0], dtype=torch.float64, device="cuda")
+    den = torch.tensor([2.0, 0.0, -1.0, 4.0, float("nan")], dtype=torch.float64, device="cuda")
+    fb = torch.tensor([10.0, 20.0, 30.0, 40.0, 50.0], dtype=torch.float64, device="cuda")
+    out = torch.empty_like(num)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _lib.check(lib.sbf_divide_with_fallback(num.data_ptr(), den.data_ptr(), fb.data_ptr(), 5,
+                                            out.data_ptr(), cnt.data_ptr(), None))
+    torch.cuda.synchronize()
+    assert cnt.item() == 3
+    np.testing.assert_array_equal(out.cpu().numpy(), [0.5, 20.0, 30.0, 1.0, 50.0])

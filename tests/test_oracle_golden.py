@@ -1,0 +1,97 @@
+"""Pin the CPU oracle against golden vectors produced by the reference itself
+(tests/golden/make_golden.py).  CPU only."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import shiftbf_oracle as O
+
+RULES = ["auto", "exact", "chernoff", "none"]
+
+
+def test_plan_table_matches_reference():
+    g = golden("plans.npz")
+    for T, sr, eps, rule, N, M in g["plans"]:
+        _, n, m = O.select_plan(T, sr, eps, RULES[int(rule)])
+        assert (n, m) == (int(N), int(M)), (T, sr, eps, rule)
+
+
+def test_n0_table_and_truncation_pins():
+    g = golden("plans.npz")
+    n0 = {int(s): int(n) for s, n in g["n0"]}
+    assert n0 == {5: 1053, 10: 263, 20: 66, 30: 29, 40: 16, 60: 7, 80: 4, 100: 3}
+    for N, e, M in g["exact"]:
+        assert O.truncation_index_exact(int(N), float(e)) == int(M)
+    for N, e, M in g["chernoff"]:
+        assert O.truncation_index_chernoff(int(N), float(e)) == int(M)
+    assert O.truncation_index_chernoff(263, 0.005) == 91
+
+
+def test_expansion_weights():
+    g = golden("expansions.npz")
+    for key in g.files:
+        if not key.startswith("w_"):
+            continue
+        N, M = map(int, key[2:].split("_"))
+        n, w, f = O.raised_cosine_terms(N, M, {2: 1.0, 29: 30.0, 229: 10.0, 263: 10.0, 2463: 800.0}[N])
+        np.testing.assert_array_equal(w, g[key])
+        np.testing.assert_array_equal(f, g["f_" + key[2:]])
+
+
+def test_max_filter_bit_exact():
+    g = golden("maxfilter.npz")
+    for k in range(40):
+        img, R = g[f"img_{k}"], int(g[f"R_{k}"])
+        assert np.array_equal(O.max_filter_2d(img, R), g[f"M_{k}"])
+        assert O.compute_T(img, R) == float(g[f"T_{k}"])
+    for k in range(20):
+        assert np.array_equal(O.max_filter_1d(g[f"seq_{k}"], int(g[f"sR_{k}"])), g[f"smax_{k}"])
+
+
+def test_brute_force_T_agrees():
+    rng = np.random.default_rng(12)
+    for _ in range(10):
+        img = rng.uniform(0, 255, (int(rng.integers(2, 30)), int(rng.integers(2, 30))))
+        R = int(rng.integers(1, 6))
+        assert O.compute_T(img, R) == O.brute_force_T(img, R)
+
+
+def test_smoothing_matches_reference():
+    g = golden("smoothing.npz")
+    for k in range(9):
+        sigma, passes = g[f"sig_{k}"]
+        r, a = O.extended_box_params(float(sigma), int(passes))
+        assert (r, a) == (int(g[f"ra_{k}"][0]), float(g[f"ra_{k}"][1]))
+        np.testing.assert_allclose(O.iterated_box(g[f"img_{k}"], float(sigma), int(passes)),
+                                   g[f"out_{k}"], rtol=1e-12, atol=1e-9)
+    for j in range(5):
+        np.testing.assert_allclose(O.box_filter(g[f"bimg_{j}"], int(g[f"brad_{j}"])),
+                                   g[f"bout_{j}"], rtol=1e-12, atol=1e-9)
+
+
+def _run_case(g, k):
+    ss, sr, eps, boxr, fT, tr = g[f"par_{k}"]
+    spatial = None if boxr < 0 else ("box", int(boxr))
+    return O.shiftable_bf(g[f"img_{k}"], float(ss), float(sr), float(eps), spatial=spatial,
+                          fixed_T=None if math.isnan(fT) else float(fT), truncation=RULES[int(tr)])
+
+
+@pytest.mark.parametrize("k", range(16))
+def test_shiftable_bf_matches_reference(k):
+    g = golden("bf_small.npz")
+    res = _run_case(g, k)
+    T, N, M, fb = g[f"plan_{k}"]
+    assert (res["T"], res["N"], res["M"], res["fallback_pixels"]) == (T, int(N), int(M), int(fb))
+    np.testing.assert_allclose(res["image"], g[f"out_{k}"], rtol=1e-9, atol=1e-7)
+
+
+def test_config1_plan_and_crop():
+    from paper_1203_5128_b200.workloads import config_image
+    g = golden("config1.npz")
+    img = config_image(1)
+    assert O.compute_T(img, 9) == 251.39522633396712
+    assert O.select_plan(251.39522633396712, 30.0, 0.01) == (251.39522633396712, 29, 7)
+    np.testing.assert_array_equal(O.max_filter_2d(img, 9)[::8, ::8], g["M"])
