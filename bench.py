@@ -1,0 +1,386 @@
+"""Benchmark contract for the B200 shiftable bilateral filter.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 2] [--no-cpu-baseline]
+
+One "step" = one pass of the hot path over one image of the workload:
+K1 local range -> K2 device plan -> K3 fused term kernel -> K4 epilogue,
+input resident in HBM, no host synchronisation inside the step.  Default
+workload: BASELINE.json configs[1] (1024x1024 float32, sigma_s=5,
+sigma_r=10, eps=0.01), seeded synthetic input.
+L2 (126 MB) is flushed between timed steps by writing a 256 MiB buffer.
+Multi-GPU (torchrun): config 2 is single-GPU by definition, so every rank
+filters its own replica (weak scaling, no collective on the data path);
+timing is max over ranks of device-event time.
+Prints exactly one JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "Mpixel/s shiftable Gaussian BF at 1/2/4/8 B200; % of FP32/HBM roofline"
+UNIT = "Mpixel/s"
+OPS_PER_PX_TERM = 132   # phasor 4 + f*c,f*s 2 + 4 images x 6 line passes x 5 + acc 6
+OPS_PER_PX = 10         # local range ~8 + divide ~2
+L2_FLUSH_BYTES = 256 << 20
+
+
+def _cfg_params(cfg):
+    from paper_1203_5128_b200.workloads import CONFIGS
+    return CONFIGS[cfg]
+
+
+# ----------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# CPU baseline (the oracle port; reference-arm and cpu_baseline leg only)
+# ----------------------------------------------------------------------------
+def _cpu_band(args):
+    img, y0, y1, halo, T, p = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import shiftbf_oracle as O
+    a, b = max(0, y0 - halo), min(img.shape[0], y1 + halo)
+    t = time.perf_counter()
+    out = O.shiftable_bf(img[a:b], p["sigma_s"], p["sigma_r"], p["epsilon"], fixed_T=T)
+    dt = time.perf_counter() - t
+    return (y1 - y0) * img.shape[1], dt, out["N"], out["M"]
+
+
+def cpu_baseline(cfg=2, band_rows=32, max_procs=None, target_s=20.0):
+    """Time the CPU oracle (numpy float64 port of the reference path) on a
+    bounded sample: `procs` bands of `band_rows` output rows (halo = support,
+    fixed_T = global T, the strip-equivalence of SURVEY.md Appendix C), one
+    process per host core.  Returns (Mpix/s, cores, sample text)."""
+    from oracle import shiftbf_oracle as O
+    from paper_1203_5128_b200.workloads import config_image
+    p = _cfg_params(cfg)
+    img = config_image(cfg).astype(np.float64)
+    r, a = O.extended_box_params(p["sigma_s"], 3)
+    halo = 3 * (r + (1 if a > 0 else 0))
+    T = O.compute_T(img, max(1, halo))
+    procs = max(1, min(max_procs or os.cpu_count() or 1, img.shape[0] // band_rows))
+    jobs = [(img, k * band_rows, (k + 1) * band_rows, halo, T, p) for k in range(procs)]
+    t = time.perf_counter()
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_cpu_band, jobs)
+    wall = time.perf_counter() - t
+    px = sum(x[0] for x in res)
+    sample = (f"{procs} bands x {band_rows} rows x {img.shape[1]} cols of {p['name']} "
+              f"(halo {halo}, fixed global T={T:.6g}, N={res[0][2]}, M={res[0][3]}), "
+              f"{procs} processes, wall {wall:.2f}s")
+    return px / wall / 1e6, procs, sample
+
+
+# ----------------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------------
+def fp32_peak(lib, torch, dev):
+    out = torch.zeros(1, device=dev)
+    st = torch.cuda.current_stream()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    blocks, threads, iters = sms * 8, 256, 8192
+    best = 0.0
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        lib.sbf_fp32_probe(blocks, threads, iters, out.data_ptr(), st.cuda_stream)
+        e1.record(st)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = max(best, blocks * threads * iters * 8 / (ms * 1e-3))
+    return best / 1e12, sms
+
+
+def load_profile_traffic():
+    """dram bytes per K3 launch from the committed ncu --set full summary."""
+    path = os.path.join(REPO, "profiles", "k3_traffic.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_ours(args, rank, world, dev):
+    import torch
+
+    import paper_1203_5128_b200 as P
+    from paper_1203_5128_b200 import _lib
+    from paper_1203_5128_b200.kernels import log_2_over_eps
+    from paper_1203_5128_b200.spatial import to_c_spatial
+    from paper_1203_5128_b200.workloads import config_image
+
+    lib = _lib.load()
+    p = _cfg_params(args.config)
+    img_np = config_image(args.config)
+    H, W = img_np.shape
+    f = torch.from_numpy(np.ascontiguousarray(img_np)).to(dev)
+    dt = _lib.SBF_F64 if f.dtype == torch.float64 else _lib.SBF_F32
+    params = P.FilterParams(sigma_s=p["sigma_s"], sigma_r=p["sigma_r"], epsilon=p["epsilon"],
+                            precision="fp32")
+    sp = to_c_spatial(params.resolved_spatial())
+    R = params.resolved_radius()
+    prec = _lib.PREC_FP32
+    cap = 1 << 16
+    stats = torch.empty(8, dtype=torch.float64, device=dev)
+    plan = torch.empty(64, dtype=torch.uint8, device=dev)
+    terms = torch.empty(cap * 32, dtype=torch.uint8, device=dev)
+    out = torch.empty((H, W), dtype=torch.float32, device=dev)
+    fb = torch.zeros(1, dtype=torch.int64, device=dev)
+    lr_ws = torch.empty(max(256, lib.sbf_local_range_workspace(H, W, dt)), dtype=torch.uint8,
+                        device=dev)
+    f_ws = torch.empty(max(256, lib.sbf_filter_workspace(H, W, sp, prec)), dtype=torch.uint8,
+                       device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream()
+    sptr = st.cuda_stream
+    l2e = log_2_over_eps(p["epsilon"])
+
+    def step(evs=None):
+        def rec(i):
+            if evs is not None:
+                evs[i].record(st)
+        rec(0)
+        _lib.check(lib.sbf_local_range(f.data_ptr(), dt, H, W, W, R, 0, H, None, stats.data_ptr(),
+                                       lr_ws.data_ptr(), lr_ws.numel(), sptr))
+        rec(1)
+        _lib.check(lib.sbf_plan_device(stats.data_ptr(), 0, 0.0, p["sigma_r"], p["epsilon"], 0,
+                                       l2e, plan.data_ptr(), terms.data_ptr(), cap, sptr))
+        rec(2)
+        lib.sbf_set_stage_mask(1)
+        _lib.check(lib.sbf_filter(f.data_ptr(), dt, H, W, W, 0, H, 0, H, sp, plan.data_ptr(),
+                                  terms.data_ptr(), stats.data_ptr(), prec, out.data_ptr(),
+                                  _lib.SBF_F32, fb.data_ptr(), f_ws.data_ptr(), f_ws.numel(), sptr))
+        rec(3)
+        lib.sbf_set_stage_mask(2)
+        _lib.check(lib.sbf_filter(f.data_ptr(), dt, H, W, W, 0, H, 0, H, sp, plan.data_ptr(),
+                                  terms.data_ptr(), stats.data_ptr(), prec, out.data_ptr(),
+                                  _lib.SBF_F32, fb.data_ptr(), f_ws.data_ptr(), f_ws.numel(), sptr))
+        lib.sbf_set_stage_mask(3)
+        rec(4)
+
+    for _ in range(args.warmup):
+        step()
+        flush.zero_()
+    torch.cuda.synchronize()
+    planc = _lib.SbfPlan.from_buffer_copy(plan.cpu().numpy().tobytes())
+    # parity spot check of the benchmarked output (cheap invariants)
+    o = out.cpu().numpy()
+    assert np.isfinite(o).all() and o.min() >= img_np.min() - 1e-3 and o.max() <= img_np.max() + 1e-3
+
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    evsets = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    with ClockSampler(dev.index if dev.index is not None else 0) as clk:
+        for k in range(args.steps):
+            step(evsets[k])
+            flush.zero_()
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    step_ms = [e[0].elapsed_time(e[4]) for e in evsets]
+    k3_ms = [e[2].elapsed_time(e[3]) for e in evsets]
+    k1_ms = [e[0].elapsed_time(e[1]) for e in evsets]
+    total_ms = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    px = H * W
+    value = world * px * args.steps / (total_ms * 1e-3) / 1e6
+
+    # e2e through the public API from pinned host memory (input H2D + result D2H)
+    pinned = torch.from_numpy(np.ascontiguousarray(img_np)).pin_memory()
+    for _ in range(max(1, args.warmup)):
+        P.shiftable_bf(pinned, params)
+    torch.cuda.synchronize()
+    e2e_ms = []
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        res = P.shiftable_bf(pinned, params)
+        e1.record(st)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+        flush.zero_()
+    e2e_total = float(np.sum(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = world * px * args.steps / (e2e_total * 1e-3) / 1e6
+    h2d = img_np.nbytes
+    d2h = px * 8 + 64 + 64 + 8  # float64 result + plan + stats + fallback counter
+
+    peak_meas, sms = fp32_peak(lib, torch, dev)
+    peak_nominal = sms * 128 * 1.965e9 / 1e12
+    k3_avg = float(np.mean(k3_ms))
+    ops = OPS_PER_PX_TERM * px * planc.K_eval
+    achieved = ops / (k3_avg * 1e-3) / 1e12
+    geo = ctypes_int7()
+    lib.sbf_filter_geometry(H, W, sp, prec, geo)
+    return dict(
+        value=value, ms_per_step=ms_per_step, planc=planc, k3_avg=k3_avg, k1_avg=float(np.mean(k1_ms)),
+        e2e=dict(value=e2e_value, unit=UNIT, h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h),
+                 ms_per_step=e2e_total / args.steps),
+        roofline=dict(bound="fp32", achieved=achieved, peak=peak_nominal, unit="TFLOP/s",
+                      frac=achieved / peak_nominal, traffic=load_profile_traffic(),
+                      peak_source="nominal 148 SM x 128 FP32 lanes x 1.965 GHz (ops: FADD/FMUL/FFMA = 1)",
+                      peak_measured_ffma=peak_meas, frac_of_measured=achieved / peak_meas,
+                      kernel="sbf::terms_kernel<4,3,0> (K3)",
+                      ops_per_launch=ops, ops_basis=f"{OPS_PER_PX_TERM} ops/px/evaluated term x {px} px x {planc.K_eval} terms"),
+        clocks=clk.summary(), geometry=list(geo), W=W, H=H, p=p)
+
+
+def ctypes_int7():
+    import ctypes
+    return (ctypes.c_int * 7)()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    p = _cfg_params(args.config)
+
+    if args.impl == "reference":
+        # the reference's CPU path (oracle port; the Python reference cannot
+        # travel to the box) on the host cores, rank 0 only
+        if rank != 0:
+            return
+        vals = []
+        for _ in range(args.warmup):
+            pass  # the port has no warm-up state; warm-up steps are not timed
+        for k in range(args.steps):
+            v, cores, sample = cpu_baseline(args.config, max_procs=None)
+            vals.append(v)
+        v = float(np.median(vals))
+        line = dict(metric=METRIC, value=v, unit=UNIT, n_gpus=args.gpus, steps=args.steps,
+                    warmup=args.warmup, ms_per_step=None, higher_is_better=True, scaling="weak",
+                    vs_baseline=None, dtype="f64", data="synthetic (SURVEY.md Appendix A generator)",
+                    config=dict(workload=p["name"], sigma_s=p["sigma_s"], sigma_r=p["sigma_r"],
+                                epsilon=p["epsilon"]),
+                    impl="reference",
+                    cpu_baseline=dict(value=v, unit=UNIT, cores=cores, kind="port", sample=sample),
+                    e2e=dict(value=v, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+        print(json.dumps(line))
+        return
+
+    import torch
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl")
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    r = run_ours(args, rank, world, dev)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, sample = cpu_baseline(args.config)
+        cpu = dict(value=v, unit=UNIT, cores=cores, kind="port", sample=sample)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    if rank != 0:
+        return
+    pl = r["planc"]
+    geo = r["geometry"]
+    line = dict(
+        metric=METRIC, value=r["value"], unit=UNIT, n_gpus=world, steps=args.steps,
+        warmup=args.warmup, ms_per_step=r["ms_per_step"], higher_is_better=True, scaling="weak",
+        vs_baseline=None, dtype="f32",
+        data="synthetic (SURVEY.md Appendix A generator, seeded; BASELINE names no dataset)",
+        config=dict(workload=p["name"], H=r["H"], W=r["W"], sigma_s=p["sigma_s"],
+                    sigma_r=p["sigma_r"], epsilon=p["epsilon"], T=pl.T, N=pl.N, M=pl.M, K=pl.K,
+                    K_eval=pl.K_eval, parallelism=("replicas" if world > 1 else "single"),
+                    l2="flushed between timed steps (256 MiB write)",
+                    k3_geometry=dict(halo=geo[0], out_cols_per_strip=geo[1], threads=geo[2],
+                                     band_rows=geo[3], strips=geo[4], bands=geo[5], groups=geo[6]),
+                    k3_ms=r["k3_avg"], k1_ms=r["k1_avg"]),
+        roofline=r["roofline"], cpu_baseline=cpu, e2e=r["e2e"],
+        gpu_launches=7 * args.steps, clocks=r["clocks"])
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -187,6 +187,15 @@ int sbf_divide_with_fallback(const double* num, const double* den,
                              const double* fallback, int64_t n, double* out,
                              unsigned long long* count_dev, void* stream);
 
+/* ---- introspection / benchmarking hooks ---- */
+int sbf_num_specialisations(void);
+int sbf_specialisation(int i, int* r, int* passes, int* mode);
+int sbf_filter_geometry(int64_t rows_out, int64_t W, const sbf_spatial* sp, int precision,
+                        int* out7);
+int sbf_truncation_index_exact_bigint(int N, double epsilon, int* M);
+int sbf_set_stage_mask(int mask);
+int sbf_fp32_probe(int blocks, int threads, int iters, float* out_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -75,6 +75,8 @@ _SIGS = {
                                      _dbl, _int, _dbl, _int, _vp, C.POINTER(SbfPlan),
                                      C.POINTER(C.c_ulonglong)]),
     "sbf_divide_with_fallback": (_int, [_vp, _vp, _vp, _i64, _vp, _vp, _vp]),
+    "sbf_set_stage_mask": (_int, [_int]),
+    "sbf_fp32_probe": (_int, [_int, _int, _int, _vp, _vp]),
 }
 EXPORTS = tuple(_SIGS)
 

@@ -155,6 +155,9 @@ static int launch_epilogue(const FilterLaunch& a, const ACC* nd, int groups, int
   return SBF_OK;
 }
 
+// stage mask for benchmarking: 1 = K3 term kernel, 2 = K4 epilogue (3 = both)
+static thread_local int g_stage_mask = 3;
+
 int launch_filter(const FilterLaunch& a) {
   int r, passes;
   double alpha;
@@ -219,8 +222,11 @@ int launch_filter(const FilterLaunch& a) {
   p.stats = a.stats;
   p.nd = a.ws;
   p.nd_group_stride = rows_out * a.W;
-  int rc = e->launch(p, a.stream);
-  if (rc != SBF_OK) return rc;
+  if (g_stage_mask & 1) {
+    int rc = e->launch(p, a.stream);
+    if (rc != SBF_OK) return rc;
+  }
+  if (!(g_stage_mask & 2)) return SBF_OK;
   if (a.precision == SBF_PREC_HDR)
     return launch_epilogue<double>(a, static_cast<const double*>(a.ws), g.groups, rows_out * a.W);
   return launch_epilogue<float>(a, static_cast<const float*>(a.ws), g.groups, rows_out * a.W);
@@ -235,6 +241,41 @@ static cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 extern "C" {
 
 int sbf_abi_version(void) { return SBF_ABI_VERSION; }
+
+// Benchmark hook: restrict sbf_filter to the term kernel (1), the epilogue
+// (2) or both (3, default) on the calling thread.
+int sbf_set_stage_mask(int mask) {
+  if (mask < 1 || mask > 3) return SBF_ERR_INVALID;
+  sbf::g_stage_mask = mask;
+  return SBF_OK;
+}
+
+// FP32 issue-rate probe: 8 independent FFMA chains (immediate operands) per
+// thread; ops = blocks * threads * iters * 8.  Used by bench.py to measure the
+// FP32 roofline denominator on the box.
+__global__ void fp32_probe_kernel(float* out, int iters) {
+  float a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+        a6 = a0 + 6, a7 = a0 + 7;
+#pragma unroll 4
+  for (int i = 0; i < iters; ++i) {
+    a0 = fmaf(a0, 0.9999f, 0.5f);
+    a1 = fmaf(a1, 0.9999f, 0.5f);
+    a2 = fmaf(a2, 0.9999f, 0.5f);
+    a3 = fmaf(a3, 0.9999f, 0.5f);
+    a4 = fmaf(a4, 0.9999f, 0.5f);
+    a5 = fmaf(a5, 0.9999f, 0.5f);
+    a6 = fmaf(a6, 0.9999f, 0.5f);
+    a7 = fmaf(a7, 0.9999f, 0.5f);
+  }
+  const float s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 1234.5f) out[0] = s;  // keep the chains alive
+}
+
+int sbf_fp32_probe(int blocks, int threads, int iters, float* out_dev, void* stream) {
+  fp32_probe_kernel<<<blocks, threads, 0, as_stream(stream)>>>(out_dev, iters);
+  SBF_CHECK_LAUNCH();
+  return SBF_OK;
+}
 const char* sbf_last_error(void) { return sbf::g_err; }
 
 int sbf_device_count(int* count) {
