@@ -90,7 +90,7 @@ def test_device_plan_matches_host_plan_and_oracle():
         nz = scale > 0
         assert sorted(tt["index"].tolist()) == sorted(idx[nz].tolist())
         order = np.argsort(tt["index"])
-        np.testing.assert_allclose(tt["scale"][order], scale[nz][np.argsort(idx[nz])], rtol=1e-12)
+        np.testing.assert_allclose(tt["scale"][order], scale[nz][np.argsort(idx[nz])], rtol=1e-12, atol=1e-300)
         np.testing.assert_array_equal(tt["freq"][order], freq[nz][np.argsort(idx[nz])])
 
 
