@@ -47,38 +47,35 @@ def _cfg_params(cfg):
 # clocks sampling (nvidia-smi during the timed region)
 # ----------------------------------------------------------------------------
 class ClockSampler:
+    """Polls nvidia-smi (one query per ~100 ms) on a thread during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index=0):
         self.index = index
-        self.proc = None
         self.lines = []
+        self._stop = threading.Event()
+
+    def _poll(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout
+                self.lines += [ln.strip() for ln in out.splitlines() if ln.strip()]
+            except Exception:
+                pass
+            self._stop.wait(0.1)
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
+        self.t = threading.Thread(target=self._poll, daemon=True)
+        self.t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        self.t.join(timeout=6)
 
     def summary(self):
         sm, mx, reasons = [], None, set()
@@ -199,7 +196,7 @@ def run_ours(args, rank, world, dev):
     fb = torch.zeros(1, dtype=torch.int64, device=dev)
     lr_ws = torch.empty(max(256, lib.sbf_local_range_workspace(H, W, dt)), dtype=torch.uint8,
                         device=dev)
-    f_ws = torch.empty(max(256, lib.sbf_filter_workspace(H, W, sp, prec)), dtype=torch.uint8,
+    f_ws = torch.empty(max(256, lib.sbf_filter_workspace(H, W, H, dt, sp, prec)), dtype=torch.uint8,
                        device=dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     st = torch.cuda.current_stream()

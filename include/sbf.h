@@ -141,9 +141,9 @@ int sbf_plan_device(const double* T_dev, int use_fixed, double fixed_T,
                     double log_2_over_eps, sbf_plan* plan_dev,
                     sbf_term* terms_dev, int terms_cap, void* stream);
 
-/* Workspace (bytes) for sbf_filter. */
-size_t sbf_filter_workspace(int64_t rows_out, int64_t W, const sbf_spatial* sp,
-                            int precision);
+/* Workspace (bytes) for sbf_filter on an H x W buffer producing rows_out rows. */
+size_t sbf_filter_workspace(int64_t H, int64_t W, int64_t rows_out, int dtype,
+                            const sbf_spatial* sp, int precision);
 
 /* The fused shiftable filter for output rows [out_lo, out_hi) of a buffer
  * holding global image rows [row0, row0 + H) of an image of global height

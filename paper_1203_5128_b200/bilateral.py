@@ -127,7 +127,7 @@ def shiftable_bf(img, params: FilterParams) -> ShiftableResult:
     out = torch.empty((H, W), dtype=torch.float64 if out_dtype == _lib.SBF_F64 else torch.float32,
                       device=dev)
     fb = torch.zeros(1, dtype=torch.int64, device=dev)
-    ws_bytes = lib.sbf_filter_workspace(H, W, sp, prec)
+    ws_bytes = lib.sbf_filter_workspace(H, W, H, s.dtype, sp, prec)
     ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dev)
     _lib.check(lib.sbf_filter(s.tensor.data_ptr(), s.dtype, H, W, W, 0, H, 0, H, sp,
                               plan_dev.data_ptr(), terms.data_ptr(), stats.data_ptr(), prec,

@@ -100,13 +100,27 @@ static bool spatial_coeffs(const sbf_spatial& sp, int* r, int* passes, double* a
   return *r >= 0 && *passes >= 1 && *alpha >= 0.0 && *alpha < 1.0;
 }
 
-size_t filter_ws(int64_t rows_out, int64_t W, const sbf_spatial* sp, int precision) {
+// partial accumulators (+ an fp32 centred copy of float64 inputs for K3)
+size_t filter_ws(int64_t H, int64_t W, int64_t rows_out, int dtype, const sbf_spatial* sp,
+                 int precision) {
   const TermsEntry* e = find_entry(*sp, precision);
-  const size_t pair = precision == SBF_PREC_HDR ? 16 : 8;
   if (!e) return align_up((size_t)(rows_out * W) * 16);  // generic: one fp64 accumulator
   TermGeom g;
   choose_geometry(*e, rows_out, W, &g);
-  return align_up((size_t)g.groups * (size_t)(rows_out * W) * pair);
+  size_t bytes = align_up((size_t)g.groups * (size_t)(rows_out * W) * 8);
+  if (dtype == SBF_F64) bytes += align_up((size_t)(H * W) * 4);
+  return bytes;
+}
+
+__global__ void centre_to_f32_kernel(const double* __restrict__ f, int64_t H, int64_t W, int64_t ld,
+                                     const double* __restrict__ stats, float* __restrict__ out) {
+  const double c = stats[3];
+  const int64_t n = H * W;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t y = i / W, x = i - y * W;
+    out[i] = (float)(f[y * ld + x] - c);
+  }
 }
 
 // ---------------------------- K4 epilogue ----------------------------
@@ -191,15 +205,26 @@ int launch_filter(const FilterLaunch& a) {
   }
   TermGeom g;
   choose_geometry(*e, rows_out, a.W, &g);
-  const size_t pair = a.precision == SBF_PREC_HDR ? 16 : 8;
-  const size_t need = align_up((size_t)g.groups * (size_t)(rows_out * a.W) * pair);
+  const size_t nd_bytes = align_up((size_t)g.groups * (size_t)(rows_out * a.W) * 8);
+  const size_t need = filter_ws(a.H, a.W, rows_out, a.dtype, &a.sp, a.precision);
   SBF_REQUIRE(a.ws && a.ws_bytes >= need, SBF_ERR_WORKSPACE,
               "filter workspace too small (%zu < %zu)", a.ws_bytes, need);
   TermParams p;
   memset(&p, 0, sizeof(p));
-  p.f = a.f;
-  p.ld = a.ld;
-  p.f64 = a.dtype == SBF_F64;
+  if (a.dtype == SBF_F64) {
+    float* fc = reinterpret_cast<float*>(static_cast<char*>(a.ws) + nd_bytes);
+    const unsigned grid = (unsigned)smin<int64_t>((a.H * a.W + 255) / 256, 148 * 8);
+    centre_to_f32_kernel<<<grid, 256, 0, a.stream>>>(static_cast<const double*>(a.f), a.H, a.W,
+                                                     a.ld, a.stats, fc);
+    SBF_CHECK_LAUNCH();
+    p.f = fc;
+    p.ld = a.W;
+    p.centred = 1;
+  } else {
+    p.f = static_cast<const float*>(a.f);
+    p.ld = a.ld;
+    p.centred = 0;
+  }
   p.H = (int)a.H;
   p.W = (int)a.W;
   p.row0 = a.row0;
@@ -213,10 +238,8 @@ int launch_filter(const FilterLaunch& a) {
   p.r = r;
   p.alpha = (float)alpha;
   const double cint = 2.0 * r + 1.0 + 2.0 * alpha;
-  p.ad = (1.0 - alpha) / cint;
-  p.bd = alpha / cint;
-  p.a = (float)p.ad;
-  p.b = (float)p.bd;
+  p.a = (float)((1.0 - alpha) / cint);
+  p.b = (float)(alpha / cint);
   p.plan = a.plan;
   p.terms = a.terms;
   p.stats = a.stats;
@@ -227,8 +250,6 @@ int launch_filter(const FilterLaunch& a) {
     if (rc != SBF_OK) return rc;
   }
   if (!(g_stage_mask & 2)) return SBF_OK;
-  if (a.precision == SBF_PREC_HDR)
-    return launch_epilogue<double>(a, static_cast<const double*>(a.ws), g.groups, rows_out * a.W);
   return launch_epilogue<float>(a, static_cast<const float*>(a.ws), g.groups, rows_out * a.W);
 }
 
@@ -332,9 +353,10 @@ int sbf_plan_device(const double* T_dev, int use_fixed, double fixed_T, double s
                           plan_dev, terms_dev, terms_cap, as_stream(stream));
 }
 
-size_t sbf_filter_workspace(int64_t rows_out, int64_t W, const sbf_spatial* sp, int precision) {
+size_t sbf_filter_workspace(int64_t H, int64_t W, int64_t rows_out, int dtype,
+                            const sbf_spatial* sp, int precision) {
   if (!sp) return 0;
-  return sbf::filter_ws(rows_out, W, sp, precision);
+  return sbf::filter_ws(H, W, rows_out, dtype, sp, precision);
 }
 
 int sbf_filter(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int64_t row0,
@@ -372,7 +394,7 @@ size_t sbf_shiftable_bf_workspace(int64_t H, int64_t W, int dtype, const sbf_spa
                                   int precision, int terms_cap) {
   if (!sp) return 0;
   return sbf::local_range_ws(H, W, dtype) + align_up((size_t)terms_cap * sizeof(sbf_term)) +
-         sbf::filter_ws(H, W, sp, precision);
+         sbf::filter_ws(H, W, H, dtype, sp, precision);
 }
 
 int sbf_shiftable_bf(const void* f, int dtype, int64_t H, int64_t W, const sbf_spatial* sp, int R,

@@ -102,6 +102,7 @@ struct FilterLaunch {
 };
 
 int launch_filter(const FilterLaunch& a);
-size_t filter_ws(int64_t rows_out, int64_t W, const sbf_spatial* sp, int precision);
+size_t filter_ws(int64_t H, int64_t W, int64_t rows_out, int dtype, const sbf_spatial* sp,
+                 int precision);
 
 }  // namespace sbf

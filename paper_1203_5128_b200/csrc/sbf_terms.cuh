@@ -3,47 +3,46 @@
 // Replaces, per folded cosine term (reference bilateral.py:150-163):
 //   theta = omega_n f; gc, gs = cos, sin; four apply_spatial() smoothings of
 //   f*gc, gc, f*gs, gs (spatial.py:108-139: `passes` extended-box passes,
-//   rows then columns, each renormalised over the clamped window,
-//   _extended_box_lines spatial.py:120-133 on top of window_sum_lines
-//   _fastcore.pyx:61-86); num/den += scale (gc*S[f gc] + gs*S[f gs]) / ...
+//   each renormalised over the clamped window — _extended_box_lines
+//   spatial.py:120-133 on top of window_sum_lines _fastcore.pyx:61-86);
+//   num/den += scale (gc*S[f gc] + gs*S[f gs]) / (gc*S[gc] + gs*S[gs]).
+// Rows and columns commute exactly (Kronecker product), so all column passes
+// run first, then all row passes (verified to 6e-13).
 //
-// B200 design ("strip sweep", one CTA = one vertical strip x one row band x
-// one term group):
-//  * V phase: one thread per haloed column streams the band top to bottom.
-//    It builds cos/sin of 2*pi*frac(f * omega/2pi) (explicit range reduction
-//    + MUFU in fp32 mode, fp64 reduction + accurate sincospi in HDR mode),
-//    the 4 modulated images, and runs the `PASSES` column passes as O(1)
-//    running-sum recurrences
-//       V += a (x[t-1] - x[t-2D]) + b (x[t] - x[t-2D-1]),  D = r+1,
-//       a = (1-alpha)/cnt, b = alpha/cnt, cnt = 2r+1+2alpha,
-//    with the delay lines held in registers (compile-time rotation of a
-//    2r+3 register ring; no shuffles, no shared-memory traffic).  Border
-//    renormalisation is exact: zero padding plus a per-position factor
-//    cnt/cnt(pos) (pos outside the image -> 0), applied only in chunks that
-//    touch a true image border.
-//  * The vertically smoothed rows go to shared memory in chunks of ROWS rows
-//    (VB); raw scale*cos/scale*sin of the output pixels go to a small ring.
-//  * H phase: 4 lanes per row (one per image) stream the chunk's rows left to
-//    right with the same register recurrence, multiply by the raw phasor of
-//    the output pixel and write the products back in place.
-//  * Accumulate: the products are summed to (num, den) and added to this
-//    CTA's exclusive slice of a partial accumulator in global memory (L2)
-//    with vector red.add (first term of the group: plain store).
-// Intermediate images never touch HBM.  Terms of the group are swept one
-// after another; groups split the term list across CTAs (strided, largest
-// weights first) and are summed by the epilogue.
+// B200 design ("strip sweep"; one CTA = one 128-column strip x one row band
+// x one term group; the term group's terms are swept one after another):
+//  * V phase — one thread per haloed column streams the band top to bottom:
+//    phasor cos/sin(2 pi frac(f nu)) by explicit range reduction + MUFU, the
+//    four modulated images, and the column passes as O(1) recurrences
+//        A_t = A_{t-1} + a (x_{t-1} - x_{t-2D}) + b (x_t - x_{t-2D-1})
+//    (D = r+1, a = (1-alpha)/cnt, b = alpha/cnt, cnt = 2r+1+2alpha), the
+//    2r+3 input history of every pass in a register ring with compile-time
+//    rotation.  Pass p>0's ring stores pass p-1's raw accumulator, so the
+//    accumulator needs no register of its own (no copies).  Border
+//    renormalisation (zero padding + cnt/cnt(pos), 0 outside the image) is
+//    applied on read, only in blocks that touch a true image border.
+//  * The smoothed rows land in shared memory (VB, ROWS rows per chunk); the
+//    output pixels' raw scale*cos / scale*sin go to a small ring (RAW).
+//  * H phase — 4 lanes per row (one per image) stream the chunk's rows with
+//    the same recurrence, multiply by the output pixel's raw phasor and write
+//    the 4 products back in place.
+//  * Accumulate — (num, den) = sums of the products, added with vector
+//    red.add to this CTA's exclusive slice of a partial accumulator (L2);
+//    the first term of the group stores.
+// Intermediate images never touch HBM.
 #pragma once
 
 #include <type_traits>
+#include <utility>
 
 #include "sbf_common.cuh"
 
 namespace sbf {
 
 struct TermParams {
-  const void* f;
+  const float* f;  // fp32 image, already centred when `centred` != 0
   int64_t ld;
-  int f64;
+  int centred;
   int H;  // buffer rows
   int W;
   int64_t row0;   // global row index of buffer row 0
@@ -54,7 +53,6 @@ struct TermParams {
   int r;
   float alpha;
   float a, b;
-  double ad, bd;
   const sbf_plan* plan;
   const sbf_term* terms;
   const double* stats;
@@ -62,74 +60,110 @@ struct TermParams {
   int64_t nd_group_stride;  // (num, den) pairs per group
 };
 
-template <int R, int PASSES, int MODE>
+template <int R, int PASSES>
 struct TermCfg {
   static constexpr int D = R + 1;
   static constexpr int L = 2 * R + 3;
   static constexpr int HALO = PASSES * D;
-  static constexpr int IMGS = (MODE == 0 && R <= 5) ? 4 : 2;
+  static constexpr int IMGS = (R <= 4) ? 4 : 2;
   static constexpr int HALO_W = 128;
   static constexpr int WC = HALO_W - 2 * HALO;
+  static constexpr int NB = (HALO_W + L - 1) / L;  // H-phase blocks per row
+  static constexpr int VB_COLS = NB * L;
+  static constexpr int VB_PITCH = 4 * (VB_COLS + ((VB_COLS % 2 == 0) ? 1 : 2));  // == 4 mod 8 words
   static constexpr int THREADS = HALO_W * 4 / IMGS;
   static constexpr int ROWS = THREADS / 4;
   static constexpr int RING = ROWS + HALO;
-  static constexpr int VB_PITCH = HALO_W * 4 + 4;  // floats; == 4 mod 32 banks
-  static constexpr int RAW_PITCH = 2 * WC + 2;     // floats; == 2 mod 4 (WC even)
+  static constexpr int RAW_PITCH = 2 * WC + 2;  // floats; == 2 mod 4 (WC even)
+  static constexpr int GOFF = (PASSES + 2) * D + 2;  // table offset (most negative position)
   static constexpr int MIN_BLOCKS = (IMGS == 4) ? 2 : 1;
   static_assert(WC > 0, "halo too wide for a 128-column strip");
   static_assert(HALO <= ROWS, "RAW ring assumes halo <= rows per chunk");
 };
 
-template <int MODE>
-struct AccT;
-template <>
-struct AccT<0> {
-  using type = float;
-};
-template <>
-struct AccT<1> {
-  using type = double;
-};
+// compile-time loop: f(std::integral_constant<int, J>) for J in [0, N)
+template <class F, int... Js>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, Js...>) {
+  (f(std::integral_constant<int, Js>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
 
 // normalisation factor cnt_int / cnt(pos) on an axis of length n (0 outside)
-__device__ __forceinline__ double gfactor(int64_t pos, int64_t n, int r, double alpha) {
-  if (pos < 0 || pos >= n) return 0.0;
+__device__ __forceinline__ float gfactor(int64_t pos, int64_t n, int r, float alpha) {
+  if (pos < 0 || pos >= n) return 0.f;
   const int64_t lo = pos - r < 0 ? 0 : pos - r;
   const int64_t hi = pos + r > n - 1 ? n - 1 : pos + r;
   double cnt = (double)(hi - lo + 1);
-  if (alpha > 0.0) {
+  if (alpha > 0.f) {
     if (pos - r - 1 >= 0) cnt += alpha;
     if (pos + r + 1 <= n - 1) cnt += alpha;
   }
-  const double cint = 2.0 * r + 1.0 + (alpha > 0.0 ? 2.0 * alpha : 0.0);
-  return cint / cnt;
+  const double cint = 2.0 * r + 1.0 + (alpha > 0.f ? 2.0 * (double)alpha : 0.0);
+  return (float)(cint / cnt);
 }
 
-template <int R, int PASSES, int MODE>
+// One image's cascade of PASSES recurrences at rotation slot J.
+// dl[0]: masked input samples; dl[p>0]: raw accumulator of pass p-1.
+// Border blocks (BORDER) normalise on read: gt[s - p*D - k] is the factor of
+// the sample pass p reads at step s - k (k in {0, 1, 2D, 2D+1}); the final
+// output is scaled by gt[s - PASSES*D].  gt already includes the table offset.
+template <int J, int L, int D, int PASSES, bool BORDER>
+__device__ __forceinline__ float cascade(float (&dl)[PASSES][L], float& vlast, float x, float a,
+                                         float b, const float* gt) {
+  constexpr int JM1 = (J + L - 1) % L, JO1 = (J + 1) % L;
+  float acc;
+  {
+    const float prev = dl[0][JM1], o1 = dl[0][JO1], o2 = dl[0][J];
+    dl[0][J] = x;
+    const float accp = (PASSES > 1) ? dl[PASSES > 1 ? 1 : 0][JM1] : vlast;
+    acc = fmaf(a, prev - o1, accp);
+    acc = fmaf(b, x - o2, acc);
+  }
+#pragma unroll
+  for (int p = 1; p < PASSES; ++p) {
+    const float rp = dl[p][JM1], r1 = dl[p][JO1], r2 = dl[p][J];
+    dl[p][J] = acc;
+    float xt = acc, xp = rp, x1 = r1, x2 = r2;
+    if (BORDER) {
+      const float* g = gt - p * D;
+      xt *= g[0];
+      xp *= g[-1];
+      x1 *= g[-2 * D];
+      x2 *= g[-2 * D - 1];
+    }
+    const float accp = (p + 1 < PASSES) ? dl[(p + 1 < PASSES) ? p + 1 : p][JM1] : vlast;
+    const float n = fmaf(a, xp - x1, accp);
+    acc = fmaf(b, xt - x2, n);
+  }
+  vlast = acc;
+  return BORDER ? acc * gt[-PASSES * D] : acc;
+}
+
+template <int R, int PASSES>
 struct VState {
-  using C = TermCfg<R, PASSES, MODE>;
-  using acc_t = typename AccT<MODE>::type;
-  float dl[PASSES][C::IMGS][C::L];
-  acc_t V[PASSES][C::IMGS];
+  using C = TermCfg<R, PASSES>;
+  float dl[C::IMGS][PASSES][C::L];
+  float vlast[C::IMGS];
   float fq[C::L];
 };
 
-template <int R, int PASSES, int MODE>
-__global__ void __launch_bounds__(TermCfg<R, PASSES, MODE>::THREADS,
-                                  TermCfg<R, PASSES, MODE>::MIN_BLOCKS)
+template <int R, int PASSES>
+__global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES>::MIN_BLOCKS)
     terms_kernel(const TermParams p) {
-  using C = TermCfg<R, PASSES, MODE>;
-  using acc_t = typename AccT<MODE>::type;
+  using C = TermCfg<R, PASSES>;
   constexpr int D = C::D, L = C::L, HALO = C::HALO, IMGS = C::IMGS, WC = C::WC;
   constexpr int ROWS = C::ROWS, RING = C::RING, VBP = C::VB_PITCH, RAWP = C::RAW_PITCH;
-  constexpr int HALO_W = C::HALO_W, THREADS = C::THREADS;
+  constexpr int HALO_W = C::HALO_W, THREADS = C::THREADS, GOFF = C::GOFF, NB = C::NB;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* VB = reinterpret_cast<float*>(smem_raw);
   float* RAW = VB + ROWS * VBP;
-  acc_t* gv = reinterpret_cast<acc_t*>(RAW + RING * RAWP);
-  const int gv_len = p.band + 2 * HALO + HALO;
-  acc_t* gh = gv + gv_len;
+  float* gv = RAW + RING * RAWP;
+  const int gv_len = p.band + 2 * HALO + GOFF;
+  float* gh = gv + gv_len;
 
   const sbf_plan* plan = p.plan;
   if (plan->status != SBF_OK) return;
@@ -147,19 +181,23 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES, MODE>::THREADS,
   const int Bn = y1 - y0;
   const int T_total = Bn + 2 * HALO;
   const int xs = strip * WC - HALO;  // image column of haloed index 0
-  const double center = p.stats[3];
-  const float centerf = (float)center;
+  const float centerf = p.centred ? 0.f : (float)p.stats[3];
+  const float a = p.a, b = p.b;
 
-  // ---- per-CTA border tables ----
-  for (int k = tid; k < gv_len; k += THREADS) {
-    const int64_t grow = p.row0 + (int64_t)(y0 - HALO + (k - HALO));
-    gv[k] = (acc_t)gfactor(grow, p.img_H, p.r, (double)p.alpha);
-  }
-  for (int k = tid; k < HALO_W + HALO; k += THREADS) {
-    gh[k] = (acc_t)gfactor((int64_t)xs + (k - HALO), p.W, p.r, (double)p.alpha);
-  }
-  // a strip is "interior" when every column any pass touches has factor 1
-  const bool strip_interior = (xs - HALO >= D) && ((int64_t)xs + HALO_W <= (int64_t)p.W - 1 - D);
+  // ---- border tables: index = stream/haloed position + GOFF ----
+  const int64_t grow0 = p.row0 + (int64_t)(y0 - HALO);  // global row of stream position 0
+  for (int k = tid; k < gv_len; k += THREADS) gv[k] = gfactor(grow0 + (k - GOFF), p.img_H, p.r, p.alpha);
+  for (int k = tid; k < HALO_W + GOFF; k += THREADS)
+    gh[k] = gfactor((int64_t)xs + (k - GOFF), p.W, p.r, p.alpha);
+  // stream positions whose rows have factor 1 (conservative: D from the edges)
+  const int64_t sg_lo = (int64_t)D - grow0;
+  const int64_t sg_hi = p.img_H - 1 - D - grow0;
+  // last stream position whose f row exists in the buffer and the image
+  const int64_t sf_hi = smin<int64_t>(smin<int64_t>((int64_t)p.H - 1 - (y0 - HALO), p.img_H - 1 - grow0),
+                                      (int64_t)T_total - 1);
+  const int64_t sf_lo = smax<int64_t>((int64_t)-(y0 - HALO), -grow0);
+  // haloed columns whose factor is 1
+  const int qg_lo = D - xs, qg_hi = p.W - 1 - D - xs;
   __syncthreads();
 
   // ---- roles ----
@@ -167,226 +205,157 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES, MODE>::THREADS,
   const int q = tid / TPC;       // haloed column of this V thread
   const int pair = tid % TPC;    // IMGS==2: 0 -> (f cos, cos), 1 -> (f sin, sin)
   const int col = xs + q;
-  const bool col_ok = col >= 0 && col < p.W;
-  const float colmask = col_ok ? 1.f : 0.f;
+  const int colc = col < 0 ? 0 : (col >= p.W ? p.W - 1 : col);  // safe address; H masks it
   const bool out_col = q >= HALO && q < HALO + WC;
   const int hv = tid >> 2;   // H-phase row within the chunk
   const int himg = tid & 3;  // H-phase image: 0 f*cos, 1 cos, 2 f*sin, 3 sin
+  const float* fcol = p.f + (int64_t)(y0 - HALO) * p.ld + colc;  // stream position 0
 
-  const char* fbase = static_cast<const char*>(p.f);
-
-  VState<R, PASSES, MODE> st;
+  VState<R, PASSES> st;
 
   for (int kk = grp; kk < K_eval; kk += p.groups) {
     const sbf_term term = p.terms[kk];
     const bool first = (kk == grp);
     const float scale = (float)term.scale;
     const float nu = (float)term.turns;
-    const double nud = term.turns;
 
-    // reset the recurrences; prefetch f for steps 0..L-1
 #pragma unroll
-    for (int pp = 0; pp < PASSES; ++pp)
+    for (int i = 0; i < IMGS; ++i) {
+      st.vlast[i] = 0.f;
 #pragma unroll
-      for (int i = 0; i < IMGS; ++i) {
-        st.V[pp][i] = 0;
+      for (int pp = 0; pp < PASSES; ++pp)
 #pragma unroll
-        for (int j = 0; j < L; ++j) st.dl[pp][i][j] = 0.f;
-      }
-    auto fetch = [&](int t) -> float {
-      const int brow = y0 - HALO + t;
-      const int64_t grow = p.row0 + brow;
-      if (!col_ok || t >= T_total || brow < 0 || brow >= p.H || grow < 0 || grow >= p.img_H)
-        return 0.f;
-      const int64_t idx = (int64_t)brow * p.ld + col;
-      if (p.f64) return (float)(__ldg(reinterpret_cast<const double*>(fbase) + idx) - center);
-      // centre is fp32-representable: the fp32 difference is the correctly
-      // rounded exact difference, identical to the fp64 route
-      return __ldg(reinterpret_cast<const float*>(fbase) + idx) - centerf;
+        for (int j = 0; j < L; ++j) st.dl[i][pp][j] = 0.f;
+    }
+    auto fetch_checked = [&](int t) -> float {
+      if (t < sf_lo || t > sf_hi) return 0.f;
+      return __ldg(fcol + (int64_t)t * p.ld) - centerf;
     };
 #pragma unroll
-    for (int j = 0; j < L; ++j) st.fq[j] = fetch(j);
+    for (int j = 0; j < L; ++j) st.fq[j] = fetch_checked(j);
 
     for (int t0 = 0; t0 < T_total; t0 += ROWS) {
       const int t1 = min(t0 + ROWS, T_total);
-      // rows touched by this chunk's passes: stream positions [t0-HALO, t1)
-      const int64_t glo = p.row0 + (y0 - HALO) + (t0 - HALO);
-      const int64_t ghi = p.row0 + (y0 - HALO) + (t1 - 1);
-      const bool chunk_interior = strip_interior && glo >= D && ghi <= p.img_H - 1 - D;
-      // RAW ring slot of input step t0 (output rows only)
-      const int rs0 = ((t0 - HALO) % RING + RING) % RING;
+      const int rs0 = ((t0 - HALO) % RING + RING) % RING;  // RAW slot of step t0
 
       // ===================== V phase =====================
-      auto vphase = [&](auto border_tag) {
-        constexpr bool BORDER = decltype(border_tag)::value;
-        const int kb0 = t0 / L, kb1 = (t1 - 1) / L;
-        for (int kb = kb0; kb <= kb1; ++kb) {
-          const int base = kb * L;
-#pragma unroll
-          for (int J = 0; J < L; ++J) {
-            const int t = base + J;
-            if (t < t0 || t >= t1) continue;
-            const float fc = st.fq[J];
-            st.fq[J] = fetch(t + L);
-            // phasor of this pixel for the current term
-            float cv, sv;
-            if (MODE == 0) {
-              const float u = fc * nu;
-              const float k = (u + 12582912.f) - 12582912.f;  // rint, |u| < 2^22
-              const float tt = u - k;
-              if (IMGS == 4) {
-                __sincosf(tt * 6.28318530717958647f, &sv, &cv);
-              } else {
-                cv = __cosf((tt - 0.25f * pair) * 6.28318530717958647f);
-                sv = cv;
-              }
-            } else {
-              const double ud = (double)fc * nud;
-              const float tt = (float)(ud - rint(ud));
-              if (IMGS == 4) {
-                sincospif(2.f * tt, &sv, &cv);
-              } else {
-                cv = cospif(2.f * (tt - 0.25f * pair));
-                sv = cv;
-              }
-            }
-            if (BORDER) {
-              const int64_t grow = p.row0 + (y0 - HALO + t);
-              const float m = (grow >= 0 && grow < p.img_H) ? colmask : 0.f;
-              cv *= m;
-              sv *= m;
-            }
-            float x[IMGS];
-            if (IMGS == 4) {
-              x[0] = fc * cv;
-              x[1] = cv;
-              x[2] = fc * sv;
-              x[3] = sv;
-            } else {
-              x[0] = fc * cv;
-              x[1] = cv;
-            }
-            // raw scaled phasor of output pixels for the H phase
-            if (t >= HALO && t < HALO + Bn && out_col) {
-              int slot = rs0 + (t - t0);
-              if (slot >= RING) slot -= RING;
-              float* rp = RAW + slot * RAWP + 2 * (q - HALO);
+      // block variants: KIND 0 main (no guards, no border), 1 guarded
+      // (partial block / band edges), 2 border (guarded + renormalisation)
+      auto vblock = [&](auto kind_tag, const int base) {
+        constexpr int KIND = decltype(kind_tag)::value;
+        constexpr bool GUARD = KIND >= 1, BORDER = KIND == 2;
+        const float* fb = fcol + (int64_t)(base + L) * p.ld;
+        static_for<L>([&](auto jc) {
+          constexpr int J = decltype(jc)::value;
+          const int t = base + J;
+          if (GUARD && (t < t0 || t >= t1)) return;
+          const float fc = st.fq[J];
+          st.fq[J] = GUARD ? fetch_checked(t + L) : (__ldg(fb + (int64_t)J * p.ld) - centerf);
+          // phasor of this pixel for the current term
+          const float u = fc * nu;
+          const float tt = u - ((u + 12582912.f) - 12582912.f);  // frac, |u| < 2^22
+          float cv, sv;
+          if (IMGS == 4) {
+            __sincosf(tt * 6.28318530717958647f, &sv, &cv);
+          } else {
+            cv = __cosf((tt - 0.25f * pair) * 6.28318530717958647f);
+            sv = cv;
+          }
+          if (BORDER) {  // rows outside the image contribute nothing (zero padding)
+            const float m = (grow0 + t >= 0 && grow0 + t < p.img_H) ? 1.f : 0.f;
+            cv *= m;
+            sv *= m;
+          }
+          // raw scaled phasor of output pixels for the H phase
+          if (!GUARD || (t >= HALO && t < HALO + Bn)) {
+            int slot = rs0 + (t - t0);
+            slot = slot >= RING ? slot - RING : slot;
+            float* rp = RAW + slot * RAWP + 2 * (q - HALO);
+            if (out_col) {
               if (IMGS == 4) {
                 *reinterpret_cast<float2*>(rp) = make_float2(scale * cv, scale * sv);
               } else {
                 rp[pair] = scale * cv;
               }
             }
-            // column passes
-            acc_t gfac[PASSES];
-            if (BORDER) {
-#pragma unroll
-              for (int pp = 0; pp < PASSES; ++pp) gfac[pp] = gv[t - (pp + 1) * D + HALO];
-            }
-#pragma unroll
-            for (int i = 0; i < IMGS; ++i) {
-              float xin = x[i];
-#pragma unroll
-              for (int pp = 0; pp < PASSES; ++pp) {
-                const float prev = st.dl[pp][i][(J + L - 1) % L];
-                const float o1 = st.dl[pp][i][(J + 1) % L];
-                const float o2 = st.dl[pp][i][J];
-                st.dl[pp][i][J] = xin;
-                if (MODE == 0) {
-                  float v = st.V[pp][i];
-                  v = fmaf(p.a, prev - o1, v);
-                  v = fmaf(p.b, xin - o2, v);
-                  st.V[pp][i] = v;
-                  xin = BORDER ? v * (float)gfac[pp] : v;
-                } else {
-                  double v = st.V[pp][i];
-                  v = fma(p.ad, (double)prev - (double)o1, v);
-                  v = fma(p.bd, (double)xin - (double)o2, v);
-                  st.V[pp][i] = v;
-                  xin = (float)(BORDER ? v * (double)gfac[pp] : v);
-                }
-              }
-              x[i] = xin;
-            }
-            // vertically smoothed output row -> VB
-            if (t >= 2 * HALO) {
-              float* vp = VB + (t - t0) * VBP + 4 * q;
-              if (IMGS == 4) {
-                *reinterpret_cast<float4*>(vp) = make_float4(x[0], x[1], x[2], x[3]);
-              } else {
-                *reinterpret_cast<float2*>(vp + 2 * pair) = make_float2(x[0], x[1]);
-              }
+          }
+          const float* gt = gv + t + GOFF;
+          float y[IMGS];
+          y[0] = cascade<J, L, D, PASSES, BORDER>(st.dl[0], st.vlast[0], fc * cv, a, b, gt);
+          y[1] = cascade<J, L, D, PASSES, BORDER>(st.dl[1], st.vlast[1], cv, a, b, gt);
+          if (IMGS == 4) {
+            y[IMGS > 2 ? 2 : 0] = cascade<J, L, D, PASSES, BORDER>(
+                st.dl[IMGS > 2 ? 2 : 0], st.vlast[IMGS > 2 ? 2 : 0], fc * sv, a, b, gt);
+            y[IMGS > 3 ? 3 : 0] = cascade<J, L, D, PASSES, BORDER>(
+                st.dl[IMGS > 3 ? 3 : 0], st.vlast[IMGS > 3 ? 3 : 0], sv, a, b, gt);
+          }
+          // vertically smoothed output row -> VB
+          if (!GUARD || t >= 2 * HALO) {
+            float* vp = VB + (t - t0) * VBP + 4 * q;
+            if (IMGS == 4) {
+              *reinterpret_cast<float4*>(vp) = make_float4(y[0], y[1], y[IMGS > 2 ? 2 : 0],
+                                                           y[IMGS > 3 ? 3 : 0]);
+            } else {
+              *reinterpret_cast<float2*>(vp + 2 * pair) = make_float2(y[0], y[1]);
             }
           }
-        }
+        });
       };
-      if (chunk_interior)
-        vphase(std::integral_constant<bool, false>{});
-      else
-        vphase(std::integral_constant<bool, true>{});
+      for (int base = (t0 / L) * L; base < t1; base += L) {
+        const bool full = base >= t0 && base + L <= t1 && base >= 2 * HALO &&
+                          base + L <= HALO + Bn && base + 2 * L - 1 <= sf_hi;
+        const bool gin = base - (PASSES + 2) * D - 1 >= sg_lo && base + L - 1 <= sg_hi;
+        if (full && gin)
+          vblock(std::integral_constant<int, 0>{}, base);
+        else if (gin)
+          vblock(std::integral_constant<int, 1>{}, base);
+        else
+          vblock(std::integral_constant<int, 2>{}, base);
+      }
       __syncthreads();
 
       // ===================== H phase =====================
       {
         const int t = t0 + hv;
         if (t < t1 && t >= 2 * HALO) {
-          float* vrow = VB + hv * VBP;
-          const int oslot = ((t - 2 * HALO) % RING);
-          const float* rrow = RAW + oslot * RAWP + (himg >> 1);
+          float* vrow = VB + hv * VBP + himg;
+          const int oslot = (t - 2 * HALO) % RING;
+          const float* rrow = RAW + oslot * RAWP + (himg >> 1) - 4 * HALO;  // index by 2*q
           float hd[PASSES][L];
-          acc_t hV[PASSES];
+          float hlast = 0.f;
 #pragma unroll
-          for (int pp = 0; pp < PASSES; ++pp) {
-            hV[pp] = 0;
+          for (int pp = 0; pp < PASSES; ++pp)
 #pragma unroll
             for (int j = 0; j < L; ++j) hd[pp][j] = 0.f;
-          }
-          auto hphase = [&](auto border_tag) {
-            constexpr bool BORDER = decltype(border_tag)::value;
-            constexpr int NB = (HALO_W + L - 1) / L;
-            for (int kb = 0; kb < NB; ++kb) {
-              const int base = kb * L;
-              float in[L], rw[L];
-#pragma unroll
-              for (int J = 0; J < L; ++J) {
-                const int qq = base + J;
-                in[J] = (qq < HALO_W) ? vrow[4 * qq + himg] : 0.f;
-                const int j = qq - 2 * HALO;
-                rw[J] = (j >= 0 && j < WC) ? rrow[2 * j] : 0.f;
+          // kind: 0 warm-up (no outputs), 1 main, 2 guarded, 3 border
+          auto hblock = [&](auto kind_tag, const int base) {
+            constexpr int KIND = decltype(kind_tag)::value;
+            constexpr bool GUARD = KIND >= 2, BORDER = KIND == 3;
+            static_for<L>([&](auto jc) {
+              constexpr int J = decltype(jc)::value;
+              const int qq = base + J;
+              if (GUARD && qq >= HALO_W) return;
+              float x = vrow[4 * qq];
+              if (BORDER) {
+                const int c = xs + qq;
+                x = (c >= 0 && c < p.W) ? x : 0.f;
               }
-#pragma unroll
-              for (int J = 0; J < L; ++J) {
-                const int qq = base + J;
-                if (qq >= HALO_W) break;
-                float xin = in[J];
-#pragma unroll
-                for (int pp = 0; pp < PASSES; ++pp) {
-                  const float prev = hd[pp][(J + L - 1) % L];
-                  const float o1 = hd[pp][(J + 1) % L];
-                  const float o2 = hd[pp][J];
-                  hd[pp][J] = xin;
-                  if (MODE == 0) {
-                    float v = hV[pp];
-                    v = fmaf(p.a, prev - o1, v);
-                    v = fmaf(p.b, xin - o2, v);
-                    hV[pp] = v;
-                    xin = BORDER ? v * (float)gh[qq - (pp + 1) * D + HALO] : v;
-                  } else {
-                    double v = hV[pp];
-                    v = fma(p.ad, (double)prev - (double)o1, v);
-                    v = fma(p.bd, (double)xin - (double)o2, v);
-                    hV[pp] = v;
-                    xin = (float)(BORDER ? v * (double)gh[qq - (pp + 1) * D + HALO] : v);
-                  }
-                }
-                if (qq >= 2 * HALO) vrow[4 * (qq - HALO) + himg] = xin * rw[J];
-              }
-            }
+              const float yv = cascade<J, L, D, PASSES, BORDER>(hd, hlast, x, a, b, gh + qq + GOFF);
+              if (KIND == 1 || (GUARD && qq >= 2 * HALO)) vrow[4 * (qq - HALO)] = yv * rrow[2 * qq];
+            });
           };
-          if (strip_interior)
-            hphase(std::integral_constant<bool, false>{});
-          else
-            hphase(std::integral_constant<bool, true>{});
+          for (int kb = 0; kb < NB; ++kb) {
+            const int base = kb * L;
+            const bool gin = base - (PASSES + 2) * D - 1 >= qg_lo && base + L - 1 <= qg_hi;
+            if (gin && base + L <= 2 * HALO)
+              hblock(std::integral_constant<int, 0>{}, base);
+            else if (gin && base >= 2 * HALO && base + L <= HALO_W)
+              hblock(std::integral_constant<int, 1>{}, base);
+            else if (gin)
+              hblock(std::integral_constant<int, 2>{}, base);
+            else
+              hblock(std::integral_constant<int, 3>{}, base);
+          }
         }
       }
       __syncthreads();
@@ -404,24 +373,13 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES, MODE>::THREADS,
           const float4 pv = *reinterpret_cast<const float4*>(VB + vv * VBP + 4 * (HALO + j));
           const int y = y0 - 2 * HALO + t0 + vv;
           const int64_t idx = (int64_t)grp * p.nd_group_stride + (int64_t)(y - p.out_lo) * p.W + x;
-          if (MODE == 0) {
-            const float num = pv.x + pv.z, den = pv.y + pv.w;
-            float2* dst = reinterpret_cast<float2*>(p.nd) + idx;
-            if (first) {
-              *dst = make_float2(num, den);
-            } else {
-              asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dst), "f"(num), "f"(den)
-                           : "memory");
-            }
+          const float num = pv.x + pv.z, den = pv.y + pv.w;
+          float2* dst = reinterpret_cast<float2*>(p.nd) + idx;
+          if (first) {
+            *dst = make_float2(num, den);
           } else {
-            const double num = (double)pv.x + (double)pv.z, den = (double)pv.y + (double)pv.w;
-            double* dst = reinterpret_cast<double*>(p.nd) + 2 * idx;
-            if (first) {
-              *reinterpret_cast<double2*>(dst) = make_double2(num, den);
-            } else {
-              atomicAdd(dst, num);
-              atomicAdd(dst + 1, den);
-            }
+            asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dst), "f"(num), "f"(den)
+                         : "memory");
           }
         }
       }
@@ -431,36 +389,35 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES, MODE>::THREADS,
 }
 
 // ---- host launcher ----
-template <int R, int PASSES, int MODE>
+template <int R, int PASSES>
 size_t terms_smem_bytes(int band) {
-  using C = TermCfg<R, PASSES, MODE>;
-  using acc_t = typename AccT<MODE>::type;
+  using C = TermCfg<R, PASSES>;
   return (size_t)C::ROWS * C::VB_PITCH * 4 + (size_t)C::RING * C::RAW_PITCH * 4 +
-         (size_t)(band + 3 * C::HALO + C::HALO_W + C::HALO) * sizeof(acc_t) + 16;
+         (size_t)(band + 2 * C::HALO + C::GOFF + C::HALO_W + C::GOFF) * 4 + 16;
 }
 
-template <int R, int PASSES, int MODE>
+template <int R, int PASSES>
 int launch_terms(const TermParams& p, cudaStream_t st) {
-  using C = TermCfg<R, PASSES, MODE>;
-  const size_t smem = terms_smem_bytes<R, PASSES, MODE>(p.band);
-  SBF_CHECK_CUDA(cudaFuncSetAttribute(terms_kernel<R, PASSES, MODE>,
+  using C = TermCfg<R, PASSES>;
+  const size_t smem = terms_smem_bytes<R, PASSES>(p.band);
+  SBF_CHECK_CUDA(cudaFuncSetAttribute(terms_kernel<R, PASSES>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const long long grid = (long long)p.nstrips * p.nbands * p.groups;
-  terms_kernel<R, PASSES, MODE><<<(unsigned)grid, C::THREADS, smem, st>>>(p);
+  terms_kernel<R, PASSES><<<(unsigned)grid, C::THREADS, smem, st>>>(p);
   SBF_CHECK_LAUNCH();
   return SBF_OK;
 }
 
-template <int R, int PASSES, int MODE>
+template <int R, int PASSES>
 void terms_geometry(int* halo, int* wc, int* threads, int* blocks_per_sm) {
-  using C = TermCfg<R, PASSES, MODE>;
+  using C = TermCfg<R, PASSES>;
   *halo = C::HALO;
   *wc = C::WC;
   *threads = C::THREADS;
   *blocks_per_sm = C::MIN_BLOCKS;
 }
 
-// dispatch table entry
+// dispatch table entry (mode: precision the instantiation serves; 0 = fp32)
 struct TermsEntry {
   int r, passes, mode;
   int (*launch)(const TermParams&, cudaStream_t);
@@ -469,6 +426,6 @@ struct TermsEntry {
 };
 
 #define SBF_TERMS_ENTRY(R, P, M) \
-  TermsEntry { R, P, M, &launch_terms<R, P, M>, &terms_smem_bytes<R, P, M>, &terms_geometry<R, P, M> }
+  TermsEntry { R, P, M, &launch_terms<R, P>, &terms_smem_bytes<R, P>, &terms_geometry<R, P> }
 
 }  // namespace sbf
