@@ -68,22 +68,7 @@ static void choose_geometry(const TermsEntry& e, int64_t rows_out, int64_t W, Te
   const int64_t band = rows_out < 512 ? rows_out : 512;
   g->band = (int)(band < 1 ? 1 : band);
   g->nbands = (int)((rows_out + g->band - 1) / g->band);
-  const double slots = (double)sm_count() * bps;
-  const double base = (double)g->nstrips * g->nbands;
-  int best = 1;
-  double best_eff = -1.0;
-  for (int G = 1; G <= 32; ++G) {
-    const double ctas = base * G;
-    const double waves = ceil(ctas / slots);
-    // a term group costs 1/G of the terms; more than ~4 waves gains nothing
-    const double eff = ctas / (waves * slots);
-    if (eff > best_eff + 0.02) {
-      best_eff = eff;
-      best = G;
-    }
-    if (ctas > 4 * slots) break;
-  }
-  g->groups = best;
+  g->groups = 1;  // persistent CTAs + work queue; one shared accumulator
   g->smem = e.smem(g->band);
 }
 
@@ -107,7 +92,7 @@ size_t filter_ws(int64_t H, int64_t W, int64_t rows_out, int dtype, const sbf_sp
   if (!e) return align_up((size_t)(rows_out * W) * 16);  // generic: one fp64 accumulator
   TermGeom g;
   choose_geometry(*e, rows_out, W, &g);
-  size_t bytes = align_up((size_t)g.groups * (size_t)(rows_out * W) * 8);
+  size_t bytes = align_up((size_t)(rows_out * W) * 8) + 256;  // accumulator + queue head
   if (dtype == SBF_F64) bytes += align_up((size_t)(H * W) * 4);
   return bytes;
 }
@@ -205,7 +190,7 @@ int launch_filter(const FilterLaunch& a) {
   }
   TermGeom g;
   choose_geometry(*e, rows_out, a.W, &g);
-  const size_t nd_bytes = align_up((size_t)g.groups * (size_t)(rows_out * a.W) * 8);
+  const size_t nd_bytes = align_up((size_t)(rows_out * a.W) * 8) + 256;
   const size_t need = filter_ws(a.H, a.W, rows_out, a.dtype, &a.sp, a.precision);
   SBF_REQUIRE(a.ws && a.ws_bytes >= need, SBF_ERR_WORKSPACE,
               "filter workspace too small (%zu < %zu)", a.ws_bytes, need);
@@ -245,6 +230,10 @@ int launch_filter(const FilterLaunch& a) {
   p.stats = a.stats;
   p.nd = a.ws;
   p.nd_group_stride = rows_out * a.W;
+  p.counter = reinterpret_cast<int*>(static_cast<char*>(a.ws) + nd_bytes - 256);
+  if (g_stage_mask & 1) {
+    SBF_CHECK_CUDA(cudaMemsetAsync(a.ws, 0, nd_bytes, a.stream));
+  }
   if (g_stage_mask & 1) {
     int rc = e->launch(p, a.stream);
     if (rc != SBF_OK) return rc;

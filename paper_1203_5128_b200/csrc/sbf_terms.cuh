@@ -9,8 +9,8 @@
 // Rows and columns commute exactly (Kronecker product), so all column passes
 // run first, then all row passes (verified to 6e-13).
 //
-// B200 design ("strip sweep"; one CTA = one 128-column strip x one row band
-// x one term group; the term group's terms are swept one after another):
+// B200 design ("strip sweep"; one work item = one 128-column strip x one row
+// band x one term):
 //  * V phase — one thread per haloed column streams the band top to bottom:
 //    phasor cos/sin(2 pi frac(f nu)) by explicit range reduction + MUFU, the
 //    four modulated images, and the column passes as O(1) recurrences
@@ -27,8 +27,9 @@
 //    the same recurrence, multiply by the output pixel's raw phasor and write
 //    the 4 products back in place.
 //  * Accumulate — (num, den) = sums of the products, added with vector
-//    red.add to this CTA's exclusive slice of a partial accumulator (L2);
-//    the first term of the group stores.
+//    red.add.v2.f32 into one zero-initialised accumulator (L2-resident).
+// Persistent CTAs (one or two per SM) pull (term, band, strip) work items
+// from an atomic counter, so border strips and short bands balance out.
 // Intermediate images never touch HBM.
 #pragma once
 
@@ -50,6 +51,7 @@ struct TermParams {
   int out_lo, out_hi;
   int band;
   int nstrips, nbands, groups;
+  int* counter;  // work-queue head (zeroed before launch)
   int r;
   float alpha;
   float a, b;
@@ -114,29 +116,32 @@ template <int J, int L, int D, int PASSES, bool BORDER>
 __device__ __forceinline__ float cascade(float (&dl)[PASSES][L], float& vlast, float x, float a,
                                          float b, const float* gt) {
   constexpr int JM1 = (J + L - 1) % L, JO1 = (J + 1) % L;
+  // The oldest sample x_{t-2D-1} lives in slot J, which the new value must
+  // overwrite: consume it first (-b x_old) so its register dies before the
+  // new value exists — the new value is then produced in place (no copies).
   float acc;
   {
     const float prev = dl[0][JM1], o1 = dl[0][JO1], o2 = dl[0][J];
-    dl[0][J] = x;
     const float accp = (PASSES > 1) ? dl[PASSES > 1 ? 1 : 0][JM1] : vlast;
-    acc = fmaf(a, prev - o1, accp);
-    acc = fmaf(b, x - o2, acc);
+    const float n = fmaf(-b, o2, fmaf(a, prev - o1, accp));
+    dl[0][J] = x;
+    acc = fmaf(b, x, n);
   }
 #pragma unroll
   for (int p = 1; p < PASSES; ++p) {
     const float rp = dl[p][JM1], r1 = dl[p][JO1], r2 = dl[p][J];
-    dl[p][J] = acc;
-    float xt = acc, xp = rp, x1 = r1, x2 = r2;
+    float xp = rp, x1 = r1, x2 = r2, gt0 = 1.f;
     if (BORDER) {
       const float* g = gt - p * D;
-      xt *= g[0];
+      gt0 = g[0];
       xp *= g[-1];
       x1 *= g[-2 * D];
       x2 *= g[-2 * D - 1];
     }
     const float accp = (p + 1 < PASSES) ? dl[(p + 1 < PASSES) ? p + 1 : p][JM1] : vlast;
-    const float n = fmaf(a, xp - x1, accp);
-    acc = fmaf(b, xt - x2, n);
+    const float n = fmaf(-b, x2, fmaf(a, xp - x1, accp));
+    dl[p][J] = acc;
+    acc = fmaf(b, BORDER ? acc * gt0 : acc, n);
   }
   vlast = acc;
   return BORDER ? acc * gt[-PASSES * D] : acc;
@@ -168,21 +173,33 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
   const sbf_plan* plan = p.plan;
   if (plan->status != SBF_OK) return;
   const int K_eval = plan->K_eval;
-  int bid = blockIdx.x;
-  const int grp = bid % p.groups;
-  bid /= p.groups;
-  const int strip = bid % p.nstrips;
-  const int band = bid / p.nstrips;
-  if (grp >= K_eval) return;
-
+  const int units = p.nstrips * p.nbands;
+  const int total = K_eval * units;
   const int tid = threadIdx.x;
+  const float centerf = p.centred ? 0.f : (float)p.stats[3];
+  const float a = p.a, b = p.b;
+  __shared__ int s_item;
+
+  VState<R, PASSES> st;
+
+  // persistent CTA: pull (term, band, strip) items, term-major, edge strips
+  // (costlier border code) first within a band
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(p.counter, 1);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= total) break;
+    const int kk = item / units;
+    const int u = item - kk * units;
+    const int band = u / p.nstrips;
+    const int si = u - band * p.nstrips;
+    const int strip = p.nstrips < 2 ? si : (si == 0 ? 0 : (si == 1 ? p.nstrips - 1 : si - 1));
+
   const int y0 = p.out_lo + band * p.band;
   const int y1 = min(p.out_hi, y0 + p.band);
   const int Bn = y1 - y0;
   const int T_total = Bn + 2 * HALO;
   const int xs = strip * WC - HALO;  // image column of haloed index 0
-  const float centerf = p.centred ? 0.f : (float)p.stats[3];
-  const float a = p.a, b = p.b;
 
   // ---- border tables: index = stream/haloed position + GOFF ----
   const int64_t grow0 = p.row0 + (int64_t)(y0 - HALO);  // global row of stream position 0
@@ -192,7 +209,7 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
   // stream positions whose rows have factor 1 (conservative: D from the edges)
   const int64_t sg_lo = (int64_t)D - grow0;
   const int64_t sg_hi = p.img_H - 1 - D - grow0;
-  // last stream position whose f row exists in the buffer and the image
+  // stream positions whose f row exists in the buffer and the image
   const int64_t sf_hi = smin<int64_t>(smin<int64_t>((int64_t)p.H - 1 - (y0 - HALO), p.img_H - 1 - grow0),
                                       (int64_t)T_total - 1);
   const int64_t sf_lo = smax<int64_t>((int64_t)-(y0 - HALO), -grow0);
@@ -211,11 +228,8 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
   const int himg = tid & 3;  // H-phase image: 0 f*cos, 1 cos, 2 f*sin, 3 sin
   const float* fcol = p.f + (int64_t)(y0 - HALO) * p.ld + colc;  // stream position 0
 
-  VState<R, PASSES> st;
-
-  for (int kk = grp; kk < K_eval; kk += p.groups) {
+  {
     const sbf_term term = p.terms[kk];
-    const bool first = (kk == grp);
     const float scale = (float)term.scale;
     const float nu = (float)term.turns;
 
@@ -227,9 +241,14 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
 #pragma unroll
         for (int j = 0; j < L; ++j) st.dl[i][pp][j] = 0.f;
     }
+    // raw samples are prefetched L steps ahead; the centre is subtracted at
+    // use so no instruction waits on the load before then
+    // rows outside [sf_lo, sf_hi] are never used unmasked: load a clamped
+    // (always valid) row instead of predicating, so nothing waits on a
+    // default-value copy into the ring register
     auto fetch_checked = [&](int t) -> float {
-      if (t < sf_lo || t > sf_hi) return 0.f;
-      return __ldg(fcol + (int64_t)t * p.ld) - centerf;
+      const int64_t tc = t < sf_lo ? sf_lo : (t > sf_hi ? sf_hi : (int64_t)t);
+      return __ldg(fcol + tc * p.ld);
     };
 #pragma unroll
     for (int j = 0; j < L; ++j) st.fq[j] = fetch_checked(j);
@@ -249,8 +268,7 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
           constexpr int J = decltype(jc)::value;
           const int t = base + J;
           if (GUARD && (t < t0 || t >= t1)) return;
-          const float fc = st.fq[J];
-          st.fq[J] = GUARD ? fetch_checked(t + L) : (__ldg(fb + (int64_t)J * p.ld) - centerf);
+          const float fc = st.fq[J] - centerf;
           // phasor of this pixel for the current term
           const float u = fc * nu;
           const float tt = u - ((u + 12582912.f) - 12582912.f);  // frac, |u| < 2^22
@@ -279,13 +297,15 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
               }
             }
           }
+          const float xfc = fc * cv, xfs = fc * sv;
+          st.fq[J] = GUARD ? fetch_checked(t + L) : __ldg(fb + (int64_t)J * p.ld);
           const float* gt = gv + t + GOFF;
           float y[IMGS];
-          y[0] = cascade<J, L, D, PASSES, BORDER>(st.dl[0], st.vlast[0], fc * cv, a, b, gt);
+          y[0] = cascade<J, L, D, PASSES, BORDER>(st.dl[0], st.vlast[0], xfc, a, b, gt);
           y[1] = cascade<J, L, D, PASSES, BORDER>(st.dl[1], st.vlast[1], cv, a, b, gt);
           if (IMGS == 4) {
             y[IMGS > 2 ? 2 : 0] = cascade<J, L, D, PASSES, BORDER>(
-                st.dl[IMGS > 2 ? 2 : 0], st.vlast[IMGS > 2 ? 2 : 0], fc * sv, a, b, gt);
+                st.dl[IMGS > 2 ? 2 : 0], st.vlast[IMGS > 2 ? 2 : 0], xfs, a, b, gt);
             y[IMGS > 3 ? 3 : 0] = cascade<J, L, D, PASSES, BORDER>(
                 st.dl[IMGS > 3 ? 3 : 0], st.vlast[IMGS > 3 ? 3 : 0], sv, a, b, gt);
           }
@@ -364,28 +384,31 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
       {
         const int vlo = max(t0, 2 * HALO) - t0;
         const int vhi = min(t1, 2 * HALO + Bn) - t0;
-        const int items = (vhi - vlo) * WC;
-        for (int it = tid; it < items; it += THREADS) {
-          const int vv = vlo + it / WC;
-          const int j = it - (it / WC) * WC;
-          const int x = strip * WC + j;
-          if (x >= p.W) continue;
-          const float4 pv = *reinterpret_cast<const float4*>(VB + vv * VBP + 4 * (HALO + j));
-          const int y = y0 - 2 * HALO + t0 + vv;
-          const int64_t idx = (int64_t)grp * p.nd_group_stride + (int64_t)(y - p.out_lo) * p.W + x;
-          const float num = pv.x + pv.z, den = pv.y + pv.w;
-          float2* dst = reinterpret_cast<float2*>(p.nd) + idx;
-          if (first) {
-            *dst = make_float2(num, den);
-          } else {
-            asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dst), "f"(num), "f"(den)
-                         : "memory");
+        const int xlim = min(WC, p.W - strip * WC);  // columns of this strip inside the image
+        constexpr int DV = THREADS / WC, DJ = THREADS % WC;
+        int vv = vlo + tid / WC, j = tid % WC;
+        float2* ndrow = reinterpret_cast<float2*>(p.nd) +
+                        (int64_t)(y0 - 2 * HALO + t0 - p.out_lo) * p.W + strip * WC;
+#pragma unroll 4
+        for (; vv < vhi;) {
+          if (j < xlim) {
+            const float4 pv = *reinterpret_cast<const float4*>(VB + vv * VBP + 4 * (HALO + j));
+            const float num = pv.x + pv.z, den = pv.y + pv.w;
+            float2* dst = ndrow + (int64_t)vv * p.W + j;
+            asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dst), "f"(num), "f"(den));
+          }
+          vv += DV;
+          j += DJ;
+          if (j >= WC) {
+            j -= WC;
+            ++vv;
           }
         }
       }
       __syncthreads();
-    }
-  }
+    }  // chunks
+  }  // term item
+  }  // work queue
 }
 
 // ---- host launcher ----
@@ -402,7 +425,10 @@ int launch_terms(const TermParams& p, cudaStream_t st) {
   const size_t smem = terms_smem_bytes<R, PASSES>(p.band);
   SBF_CHECK_CUDA(cudaFuncSetAttribute(terms_kernel<R, PASSES>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const long long grid = (long long)p.nstrips * p.nbands * p.groups;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long grid = (long long)sms * C::MIN_BLOCKS;  // persistent CTAs
   terms_kernel<R, PASSES><<<(unsigned)grid, C::THREADS, smem, st>>>(p);
   SBF_CHECK_LAUNCH();
   return SBF_OK;
