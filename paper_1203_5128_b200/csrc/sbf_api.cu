@@ -281,8 +281,33 @@ __global__ void fp32_probe_kernel(float* out, int iters) {
   if (s == 1234.5f) out[0] = s;  // keep the chains alive
 }
 
+// same with packed FFMA2 (fma.rn.f32x2, sm_100): ops = blocks*threads*iters*16
+__global__ void fp32x2_probe_kernel(float* out, int iters) {
+  float2 a0 = make_float2(threadIdx.x, 1), a1 = make_float2(2, 3), a2 = make_float2(4, 5),
+         a3 = make_float2(6, 7), a4 = make_float2(8, 9), a5 = make_float2(10, 11),
+         a6 = make_float2(12, 13), a7 = make_float2(14, 15);
+  const float2 m = make_float2(0.9999f, 0.9999f), c = make_float2(0.5f, 0.5f);
+#pragma unroll 4
+  for (int i = 0; i < iters; ++i) {
+    a0 = __ffma2_rn(a0, m, c);
+    a1 = __ffma2_rn(a1, m, c);
+    a2 = __ffma2_rn(a2, m, c);
+    a3 = __ffma2_rn(a3, m, c);
+    a4 = __ffma2_rn(a4, m, c);
+    a5 = __ffma2_rn(a5, m, c);
+    a6 = __ffma2_rn(a6, m, c);
+    a7 = __ffma2_rn(a7, m, c);
+  }
+  const float s = a0.x + a1.x + a2.x + a3.x + a4.x + a5.x + a6.x + a7.x + a0.y + a7.y;
+  if (s == 1234.5f) out[0] = s;
+}
+
 int sbf_fp32_probe(int blocks, int threads, int iters, float* out_dev, void* stream) {
-  fp32_probe_kernel<<<blocks, threads, 0, as_stream(stream)>>>(out_dev, iters);
+  if (iters < 0) {
+    fp32x2_probe_kernel<<<blocks, threads, 0, as_stream(stream)>>>(out_dev, -iters);
+  } else {
+    fp32_probe_kernel<<<blocks, threads, 0, as_stream(stream)>>>(out_dev, iters);
+  }
   SBF_CHECK_LAUNCH();
   return SBF_OK;
 }

@@ -147,11 +147,46 @@ __device__ __forceinline__ float cascade(float (&dl)[PASSES][L], float& vlast, f
   return BORDER ? acc * gt[-PASSES * D] : acc;
 }
 
+// Packed twin of `cascade`: two images per float2 (FADD2/FFMA2/FMUL2, sm_100),
+// half the FP32 instructions for the same arithmetic.
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+template <int J, int L, int D, int PASSES, bool BORDER>
+__device__ __forceinline__ float2 cascade2(float2 (&dl)[PASSES][L], float2& vlast, float2 x,
+                                           float2 a2, float2 nb2, float2 b2, const float* gt) {
+  constexpr int JM1 = (J + L - 1) % L, JO1 = (J + 1) % L;
+  float2 acc;
+  {
+    const float2 prev = dl[0][JM1], o1 = dl[0][JO1], o2 = dl[0][J];
+    const float2 accp = (PASSES > 1) ? dl[PASSES > 1 ? 1 : 0][JM1] : vlast;
+    const float2 n = __ffma2_rn(nb2, o2, __ffma2_rn(a2, __fadd2_rn(prev, make_float2(-o1.x, -o1.y)), accp));
+    dl[0][J] = x;
+    acc = __ffma2_rn(b2, x, n);
+  }
+#pragma unroll
+  for (int p = 1; p < PASSES; ++p) {
+    float2 xp = dl[p][JM1], x1 = dl[p][JO1], x2 = dl[p][J];
+    float2 gt0 = f2(1.f);
+    if (BORDER) {
+      const float* g = gt - p * D;
+      gt0 = f2(g[0]);
+      xp = __fmul2_rn(xp, f2(g[-1]));
+      x1 = __fmul2_rn(x1, f2(g[-2 * D]));
+      x2 = __fmul2_rn(x2, f2(g[-2 * D - 1]));
+    }
+    const float2 accp = (p + 1 < PASSES) ? dl[(p + 1 < PASSES) ? p + 1 : p][JM1] : vlast;
+    const float2 n = __ffma2_rn(nb2, x2, __ffma2_rn(a2, __fadd2_rn(xp, make_float2(-x1.x, -x1.y)), accp));
+    dl[p][J] = acc;
+    acc = __ffma2_rn(b2, BORDER ? __fmul2_rn(acc, gt0) : acc, n);
+  }
+  vlast = acc;
+  return BORDER ? __fmul2_rn(acc, f2(gt[-PASSES * D])) : acc;
+}
+
 template <int R, int PASSES>
 struct VState {
   using C = TermCfg<R, PASSES>;
-  float dl[C::IMGS][PASSES][C::L];
-  float vlast[C::IMGS];
+  float2 dl[C::IMGS / 2][PASSES][C::L];  // image pairs
+  float2 vlast[C::IMGS / 2];
   float fq[C::L];
 };
 
@@ -225,7 +260,7 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
   const int colc = col < 0 ? 0 : (col >= p.W ? p.W - 1 : col);  // safe address; H masks it
   const bool out_col = q >= HALO && q < HALO + WC;
   const int hv = tid >> 2;   // H-phase row within the chunk
-  const int himg = tid & 3;  // H-phase image: 0 f*cos, 1 cos, 2 f*sin, 3 sin
+  const int himg = tid & 3;  // H-phase image (VB component)
   const float* fcol = p.f + (int64_t)(y0 - HALO) * p.ld + colc;  // stream position 0
 
   {
@@ -234,12 +269,12 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
     const float nu = (float)term.turns;
 
 #pragma unroll
-    for (int i = 0; i < IMGS; ++i) {
-      st.vlast[i] = 0.f;
+    for (int i = 0; i < IMGS / 2; ++i) {
+      st.vlast[i] = f2(0.f);
 #pragma unroll
       for (int pp = 0; pp < PASSES; ++pp)
 #pragma unroll
-        for (int j = 0; j < L; ++j) st.dl[i][pp][j] = 0.f;
+        for (int j = 0; j < L; ++j) st.dl[i][pp][j] = f2(0.f);
     }
     // raw samples are prefetched L steps ahead; the centre is subtracted at
     // use so no instruction waits on the load before then
@@ -297,26 +332,26 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
               }
             }
           }
-          const float xfc = fc * cv, xfs = fc * sv;
           st.fq[J] = GUARD ? fetch_checked(t + L) : __ldg(fb + (int64_t)J * p.ld);
           const float* gt = gv + t + GOFF;
-          float y[IMGS];
-          y[0] = cascade<J, L, D, PASSES, BORDER>(st.dl[0], st.vlast[0], xfc, a, b, gt);
-          y[1] = cascade<J, L, D, PASSES, BORDER>(st.dl[1], st.vlast[1], cv, a, b, gt);
+          const float2 a2 = f2(a), nb2 = f2(-b), b2 = f2(b);
           if (IMGS == 4) {
-            y[IMGS > 2 ? 2 : 0] = cascade<J, L, D, PASSES, BORDER>(
-                st.dl[IMGS > 2 ? 2 : 0], st.vlast[IMGS > 2 ? 2 : 0], xfs, a, b, gt);
-            y[IMGS > 3 ? 3 : 0] = cascade<J, L, D, PASSES, BORDER>(
-                st.dl[IMGS > 3 ? 3 : 0], st.vlast[IMGS > 3 ? 3 : 0], sv, a, b, gt);
-          }
-          // vertically smoothed output row -> VB
-          if (!GUARD || t >= 2 * HALO) {
-            float* vp = VB + (t - t0) * VBP + 4 * q;
-            if (IMGS == 4) {
-              *reinterpret_cast<float4*>(vp) = make_float4(y[0], y[1], y[IMGS > 2 ? 2 : 0],
-                                                           y[IMGS > 3 ? 3 : 0]);
-            } else {
-              *reinterpret_cast<float2*>(vp + 2 * pair) = make_float2(y[0], y[1]);
+            // pairs: A = (f cos, f sin) -> (F_c, F_s); B = (cos, sin) -> (G_c, G_s)
+            const float2 ya = cascade2<J, L, D, PASSES, BORDER>(
+                st.dl[0], st.vlast[0], __fmul2_rn(f2(fc), make_float2(cv, sv)), a2, nb2, b2, gt);
+            const float2 yb = cascade2<J, L, D, PASSES, BORDER>(
+                st.dl[IMGS / 2 - 1], st.vlast[IMGS / 2 - 1], make_float2(cv, sv), a2, nb2, b2, gt);
+            if (!GUARD || t >= 2 * HALO) {
+              float* vp = VB + (t - t0) * VBP + 4 * q;
+              *reinterpret_cast<float4*>(vp) = make_float4(ya.x, ya.y, yb.x, yb.y);
+            }
+          } else {
+            // one pair per thread: (f v, v), v = cos (pair 0) or sin (pair 1)
+            const float2 y = cascade2<J, L, D, PASSES, BORDER>(
+                st.dl[0], st.vlast[0], __fmul2_rn(make_float2(fc, 1.f), f2(cv)), a2, nb2, b2, gt);
+            if (!GUARD || t >= 2 * HALO) {
+              float* vp = VB + (t - t0) * VBP + 4 * q;
+              *reinterpret_cast<float2*>(vp + 2 * pair) = y;
             }
           }
         });
@@ -340,7 +375,9 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
         if (t < t1 && t >= 2 * HALO) {
           float* vrow = VB + hv * VBP + himg;
           const int oslot = (t - 2 * HALO) % RING;
-          const float* rrow = RAW + oslot * RAWP + (himg >> 1) - 4 * HALO;  // index by 2*q
+          // VB image order: IMGS==4 [F_c, F_s, G_c, G_s]; IMGS==2 [F_c, G_c, F_s, G_s]
+          const int rc = (IMGS == 4) ? (himg & 1) : (himg >> 1);  // 0 -> cos, 1 -> sin
+          const float* rrow = RAW + oslot * RAWP + rc - 4 * HALO;  // index by 2*q
           float hd[PASSES][L];
           float hlast = 0.f;
 #pragma unroll
@@ -393,7 +430,8 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
         for (; vv < vhi;) {
           if (j < xlim) {
             const float4 pv = *reinterpret_cast<const float4*>(VB + vv * VBP + 4 * (HALO + j));
-            const float num = pv.x + pv.z, den = pv.y + pv.w;
+            const float num = (IMGS == 4) ? pv.x + pv.y : pv.x + pv.z;
+            const float den = (IMGS == 4) ? pv.z + pv.w : pv.y + pv.w;
             float2* dst = ndrow + (int64_t)vv * p.W + j;
             asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dst), "f"(num), "f"(den));
           }
