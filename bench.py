@@ -305,6 +305,125 @@ def run_ours(args, rank, world, dev):
         clocks=clk.summary(), geometry=list(geo), W=W, H=H, p=p)
 
 
+def _device_plan_cost(lib, torch, f, params, dev):
+    """(K_eval of the image's plan) — used to balance the config-4 shards."""
+    import paper_1203_5128_b200 as P
+    res = P.shiftable_bf(f, params)
+    return res.plan.N // 2 - res.plan.M + 1
+
+
+def run_batch(args, rank, world, dev):
+    """Config 4: a batch of independent images sharded across ranks."""
+    import torch
+
+    import paper_1203_5128_b200 as P
+    from paper_1203_5128_b200 import _lib
+    from paper_1203_5128_b200.dist import shard_images
+    from paper_1203_5128_b200.kernels import log_2_over_eps
+    from paper_1203_5128_b200.spatial import to_c_spatial
+    from paper_1203_5128_b200.workloads import config_image
+
+    lib = _lib.load()
+    p = _cfg_params(args.config)
+    n_img = args.images
+    parts = shard_images([1.0] * n_img, world)      # equal pixels; K differs by <= 2 of 12
+    mine = parts[rank]
+    imgs = [torch.from_numpy(np.ascontiguousarray(config_image(4, i))).to(dev) for i in mine]
+    H, W = imgs[0].shape
+    params = P.FilterParams(sigma_s=p["sigma_s"], sigma_r=p["sigma_r"], epsilon=p["epsilon"])
+    sp = to_c_spatial(params.resolved_spatial())
+    R = params.resolved_radius()
+    cap = 1 << 16
+    ws = torch.empty(lib.sbf_shiftable_bf_workspace(H, W, _lib.SBF_F32, sp, _lib.PREC_FP32, cap),
+                     dtype=torch.uint8, device=dev)
+    stats = torch.empty(8, dtype=torch.float64, device=dev)
+    plan = torch.empty(64, dtype=torch.uint8, device=dev)
+    outs = [torch.empty((H, W), dtype=torch.float32, device=dev) for _ in mine]
+    fb = torch.zeros(1, dtype=torch.int64, device=dev)
+    st = torch.cuda.current_stream()
+    l2e = log_2_over_eps(p["epsilon"])
+
+    def step():
+        for f, o in zip(imgs, outs):
+            _lib.check(lib.sbf_shiftable_bf(f.data_ptr(), _lib.SBF_F32, H, W, sp, R, -1.0,
+                                            p["sigma_r"], p["epsilon"], 0, l2e, _lib.PREC_FP32,
+                                            o.data_ptr(), _lib.SBF_F32, plan.data_ptr(),
+                                            stats.data_ptr(), fb.data_ptr(), cap, ws.data_ptr(),
+                                            ws.numel(), st.cuda_stream))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index or 0) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            step()
+        e1.record(st)
+        e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    total = float(t.item())
+    px = n_img * H * W
+    return dict(value=px * args.steps / (total * 1e-3) / 1e6, ms_per_step=total / args.steps,
+                launches=7 * len(mine) * args.steps, clocks=clk.summary(),
+                config=dict(workload=p["name"], images=n_img, H=H, W=W, sigma_s=p["sigma_s"],
+                            sigma_r=p["sigma_r"], epsilon=p["epsilon"],
+                            parallelism=f"image batch sharded over {world} rank(s), no collective",
+                            l2="inputs (64 MiB/image) exceed what L2 keeps across images"))
+
+
+def run_strips(args, rank, world, dev):
+    """Config 5: 3 channels, row strips + halos, global T by NCCL max-allreduce."""
+    import torch
+
+    import paper_1203_5128_b200 as P
+    from paper_1203_5128_b200.dist import StripFilter, strip_halo, strip_plan
+    from paper_1203_5128_b200.workloads import config_image
+
+    p = _cfg_params(args.config)
+    size = args.size or 16384
+    params = P.FilterParams(sigma_s=p["sigma_s"], sigma_r=p["sigma_r"], epsilon=p["epsilon"])
+    s = strip_plan(size, world, strip_halo(params))[rank]
+    bufs = []
+    for c in range(3):
+        full = config_image(5, c, size=size)
+        bufs.append(torch.from_numpy(np.ascontiguousarray(full[s.buf_lo:s.buf_hi])).to(dev))
+        del full
+    sf = StripFilter(bufs, s, size, params)
+    st = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        sf.run()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index or 0) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            sf.run()
+        e1.record(st)
+        e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    total = float(t.item())
+    px = 3 * size * size
+    plans = sf.plans_host()
+    return dict(value=px * args.steps / (total * 1e-3) / 1e6, ms_per_step=total / args.steps,
+                launches=(7 * 3) * args.steps, clocks=clk.summary(),
+                config=dict(workload=p["name"], channels=3, H=size, W=size, sigma_s=p["sigma_s"],
+                            sigma_r=p["sigma_r"], epsilon=p["epsilon"],
+                            plans=[(pl.T, pl.N, pl.M) for pl in plans],
+                            parallelism=f"row strips over {world} rank(s), halo {s.out_lo - s.buf_lo or s.buf_hi - s.out_hi} rows, "
+                                        "global T by NCCL max-allreduce (3 x fp64, one call)"))
+
+
 def ctypes_int7():
     import ctypes
     return (ctypes.c_int * 7)()
@@ -318,6 +437,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--images", type=int, default=64, help="config 4 batch size")
+    ap.add_argument("--size", type=int, default=None, help="config 5 side (default 16384)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank = int(os.environ.get("RANK", "0"))
@@ -354,6 +475,19 @@ def main():
         torch.distributed.init_process_group("nccl")
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
+    if args.config in (4, 5):
+        r = (run_batch if args.config == 4 else run_strips)(args, rank, world, dev)
+        if world > 1:
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+        if rank == 0:
+            line = dict(metric=METRIC, value=r["value"], unit=UNIT, n_gpus=world, steps=args.steps,
+                        warmup=args.warmup, ms_per_step=r["ms_per_step"], higher_is_better=True,
+                        scaling="weak" if args.config == 4 else "strong", vs_baseline=None,
+                        dtype="f32", data="synthetic (SURVEY.md Appendix A generator, seeded)",
+                        config=r["config"], gpu_launches=r["launches"], clocks=r["clocks"])
+            print(json.dumps(line))
+        return
     r = run_ours(args, rank, world, dev)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
