@@ -483,7 +483,7 @@ def main():
         if rank == 0:
             line = dict(metric=METRIC, value=r["value"], unit=UNIT, n_gpus=world, steps=args.steps,
                         warmup=args.warmup, ms_per_step=r["ms_per_step"], higher_is_better=True,
-                        scaling="weak" if args.config == 4 else "strong", vs_baseline=None,
+                        scaling="strong", vs_baseline=None,
                         dtype="f32", data="synthetic (SURVEY.md Appendix A generator, seeded)",
                         config=r["config"], gpu_launches=r["launches"], clocks=r["clocks"])
             print(json.dumps(line))
