@@ -187,8 +187,16 @@ struct VState {
   using C = TermCfg<R, PASSES>;
   float2 dl[C::IMGS / 2][PASSES][C::L];  // image pairs
   float2 vlast[C::IMGS / 2];
-  float fq[C::L];
 };
+
+// cp.async (LDGSTS) helpers for the f prefetch ring in shared memory
+__device__ __forceinline__ void cp_async_f32(float* dst_smem, const float* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int R, int PASSES>
 __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES>::MIN_BLOCKS)
@@ -204,6 +212,7 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
   float* gv = RAW + RING * RAWP;
   const int gv_len = p.band + 2 * HALO + GOFF;
   float* gh = gv + gv_len;
+  float* FR = gh + HALO_W + GOFF;  // per-thread ring of prefetched f samples (L slots)
 
   const sbf_plan* plan = p.plan;
   if (plan->status != SBF_OK) return;
@@ -278,15 +287,19 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
     }
     // raw samples are prefetched L steps ahead; the centre is subtracted at
     // use so no instruction waits on the load before then
-    // rows outside [sf_lo, sf_hi] are never used unmasked: load a clamped
-    // (always valid) row instead of predicating, so nothing waits on a
-    // default-value copy into the ring register
-    auto fetch_checked = [&](int t) -> float {
+    // f for step t is copied asynchronously (cp.async) into FR[tid][t % L],
+    // L steps ahead; every executed step commits exactly one group, so the
+    // sample of step t is the group committed L groups earlier.  Rows outside
+    // [sf_lo, sf_hi] are never used unmasked: a clamped row is loaded instead.
+    float* fr = FR + tid * L;
+    auto fetch_async = [&](int t, int slot) {
       const int64_t tc = t < sf_lo ? sf_lo : (t > sf_hi ? sf_hi : (int64_t)t);
-      return __ldg(fcol + tc * p.ld);
+      cp_async_f32(fr + slot, fcol + tc * p.ld);
+      cp_async_commit();
     };
+    cp_async_wait<0>();  // previous term's tail copies landed before slots are reused
 #pragma unroll
-    for (int j = 0; j < L; ++j) st.fq[j] = fetch_checked(j);
+    for (int j = 0; j < L; ++j) fetch_async(j, j);
 
     for (int t0 = 0; t0 < T_total; t0 += ROWS) {
       const int t1 = min(t0 + ROWS, T_total);
@@ -303,7 +316,8 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
           constexpr int J = decltype(jc)::value;
           const int t = base + J;
           if (GUARD && (t < t0 || t >= t1)) return;
-          const float fc = st.fq[J] - centerf;
+          cp_async_wait<L - 1>();
+          const float fc = fr[J] - centerf;
           // phasor of this pixel for the current term
           const float u = fc * nu;
           const float tt = u - ((u + 12582912.f) - 12582912.f);  // frac, |u| < 2^22
@@ -332,7 +346,12 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
               }
             }
           }
-          st.fq[J] = GUARD ? fetch_checked(t + L) : __ldg(fb + (int64_t)J * p.ld);
+          if (GUARD) {
+            fetch_async(t + L, J);
+          } else {
+            cp_async_f32(fr + J, fb + (int64_t)J * p.ld);
+            cp_async_commit();
+          }
           const float* gt = gv + t + GOFF;
           const float2 a2 = f2(a), nb2 = f2(-b), b2 = f2(b);
           if (IMGS == 4) {
@@ -454,7 +473,8 @@ template <int R, int PASSES>
 size_t terms_smem_bytes(int band) {
   using C = TermCfg<R, PASSES>;
   return (size_t)C::ROWS * C::VB_PITCH * 4 + (size_t)C::RING * C::RAW_PITCH * 4 +
-         (size_t)(band + 2 * C::HALO + C::GOFF + C::HALO_W + C::GOFF) * 4 + 16;
+         (size_t)(band + 2 * C::HALO + C::GOFF + C::HALO_W + C::GOFF) * 4 +
+         (size_t)C::THREADS * C::L * 4 + 16;
 }
 
 template <int R, int PASSES>
