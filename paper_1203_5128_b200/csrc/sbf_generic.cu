@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "sbf_common.cuh"
+#include "sbf_generic_fused.cuh"
 
 namespace sbf {
 namespace {
@@ -33,6 +34,39 @@ __global__ void gen_images(const void* f, int f64, int64_t H, int64_t W, int64_t
     planes[n + i] = c;
     planes[2 * n + i] = fc * s;
     planes[3 * n + i] = s;
+  }
+}
+
+// same images written transposed: planes[pl][x][y]
+__global__ void gen_images_T(const void* f, int f64, int64_t H, int64_t W, int64_t ld,
+                             const double* stats, double turns, double* planes) {
+  __shared__ double tile[4][32][33];
+  const int64_t n = H * W;
+  const double center = stats[3];
+  const int64_t x0 = (int64_t)blockIdx.x * 32, y0 = (int64_t)blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t y = y0 + k, x = x0 + threadIdx.x;
+    if (y < H && x < W) {
+      const double fv = f64 ? static_cast<const double*>(f)[y * ld + x]
+                            : (double)static_cast<const float*>(f)[y * ld + x];
+      const double fc = fv - center;
+      const double u = fc * turns;
+      const double t = u - rint(u);
+      double s, c;
+      sincospi(2.0 * t, &s, &c);
+      tile[0][k][threadIdx.x] = fc * c;
+      tile[1][k][threadIdx.x] = c;
+      tile[2][k][threadIdx.x] = fc * s;
+      tile[3][k][threadIdx.x] = s;
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t x = x0 + k, y = y0 + threadIdx.x;
+    if (x < W && y < H) {
+#pragma unroll
+      for (int pl = 0; pl < 4; ++pl) planes[pl * n + x * H + y] = tile[pl][threadIdx.x][k];
+    }
   }
 }
 
@@ -153,18 +187,54 @@ int launch_generic_terms(const FilterLaunch& a, double* nd) {
   const unsigned gpix = (unsigned)smin<int64_t>((n + bs - 1) / bs, 148 * 16);
   const int passes = a.sp.mode == SBF_SPATIAL_BOX ? 1 : a.sp.passes;
   const double alpha = a.sp.mode == SBF_SPATIAL_BOX ? 0.0 : a.sp.alpha;
-  for (int k = 0; k < plan.K_eval; ++k) {
-    gen_images<<<gpix, bs, 0, st>>>(a.f, a.dtype == SBF_F64, H, W, a.ld, a.stats,
-                                    terms[k].turns, planes);
-    for (int ps = 0; ps < passes; ++ps) {
-      gen_rows<<<(unsigned)((4 * H + bs - 1) / bs), bs, 0, st>>>(planes, tmp, 4 * H, W, a.sp.r,
-                                                                 alpha);
-      gen_cols<<<(unsigned)((4 * W + bs - 1) / bs), bs, 0, st>>>(tmp, planes, 4, H, W, a.row0,
-                                                                 a.img_H, a.sp.r, alpha);
+  const FusedEntry* fe = nullptr;
+  static const FusedEntry fused[] = {
+      {0, &launch_colpass<0>},   {1, &launch_colpass<1>},   {2, &launch_colpass<2>},
+      {3, &launch_colpass<3>},   {4, &launch_colpass<4>},   {5, &launch_colpass<5>},
+      {6, &launch_colpass<6>},   {7, &launch_colpass<7>},   {8, &launch_colpass<8>},
+      {9, &launch_colpass<9>},   {10, &launch_colpass<10>}, {11, &launch_colpass<11>},
+      {12, &launch_colpass<12>}};
+  if (passes == 3 && a.sp.r >= 0 && a.sp.r <= 12) fe = &fused[a.sp.r];
+  if (fe) {
+    // fused 3-pass cascade: rows on transposed planes, then columns
+    const int r = a.sp.r, pad = 3 * (r + 1) + 2 * (r + 1) + 2;
+    const double cint = 2.0 * r + 1.0 + 2.0 * alpha;
+    const double ca = (1.0 - alpha) / cint, cb = alpha / cint;
+    double *gx = nullptr, *gy = nullptr;
+    SBF_CHECK_CUDA(cudaMallocAsync(&gx, sizeof(double) * (W + 2 * pad), st));
+    SBF_CHECK_CUDA(cudaMallocAsync(&gy, sizeof(double) * (H + 2 * pad), st));
+    gfactor_table<<<(unsigned)((W + 2 * pad + 255) / 256), 256, 0, st>>>(gx, W, 0, W, r, alpha, pad);
+    gfactor_table<<<(unsigned)((H + 2 * pad + 255) / 256), 256, 0, st>>>(gy, H, a.row0, a.img_H, r,
+                                                                        alpha, pad);
+    const dim3 tb(32, 8), tgrid((unsigned)((W + 31) / 32), (unsigned)((H + 31) / 32), 1);
+    const dim3 tgridT((unsigned)((H + 31) / 32), (unsigned)((W + 31) / 32), 4);
+    const int64_t seg = 256;
+    for (int k = 0; k < plan.K_eval; ++k) {
+      gen_images_T<<<tgrid, tb, 0, st>>>(a.f, a.dtype == SBF_F64, H, W, a.ld, a.stats,
+                                         terms[k].turns, tmp);           // [pl][W][H]
+      fe->launch(tmp, planes, 4, W, H, seg, gx, 0, W, ca, cb, st);       // row passes
+      transpose_planes<<<tgridT, tb, 0, st>>>(planes, tmp, W, H);        // -> [pl][H][W]
+      fe->launch(tmp, planes, 4, H, W, seg, gy, a.row0, a.img_H, ca, cb, st);  // column passes
+      gen_accum<<<gpix, bs, 0, st>>>(planes, a.f, a.dtype == SBF_F64, H, W, a.ld, a.out_lo,
+                                     a.out_hi, a.stats, terms[k].turns, terms[k].scale, k == 0, nd);
+      SBF_CHECK_LAUNCH();
     }
-    gen_accum<<<gpix, bs, 0, st>>>(planes, a.f, a.dtype == SBF_F64, H, W, a.ld, a.out_lo,
-                                   a.out_hi, a.stats, terms[k].turns, terms[k].scale, k == 0, nd);
-    SBF_CHECK_LAUNCH();
+    SBF_CHECK_CUDA(cudaFreeAsync(gx, st));
+    SBF_CHECK_CUDA(cudaFreeAsync(gy, st));
+  } else {
+    for (int k = 0; k < plan.K_eval; ++k) {
+      gen_images<<<gpix, bs, 0, st>>>(a.f, a.dtype == SBF_F64, H, W, a.ld, a.stats,
+                                      terms[k].turns, planes);
+      for (int ps = 0; ps < passes; ++ps) {
+        gen_rows<<<(unsigned)((4 * H + bs - 1) / bs), bs, 0, st>>>(planes, tmp, 4 * H, W, a.sp.r,
+                                                                   alpha);
+        gen_cols<<<(unsigned)((4 * W + bs - 1) / bs), bs, 0, st>>>(tmp, planes, 4, H, W, a.row0,
+                                                                   a.img_H, a.sp.r, alpha);
+      }
+      gen_accum<<<gpix, bs, 0, st>>>(planes, a.f, a.dtype == SBF_F64, H, W, a.ld, a.out_lo,
+                                     a.out_hi, a.stats, terms[k].turns, terms[k].scale, k == 0, nd);
+      SBF_CHECK_LAUNCH();
+    }
   }
   SBF_CHECK_CUDA(cudaFreeAsync(planes, st));
   SBF_CHECK_CUDA(cudaFreeAsync(tmp, st));
