@@ -22,7 +22,7 @@
 //    renormalisation (zero padding + cnt/cnt(pos), 0 outside the image) is
 //    applied on read, only in blocks that touch a true image border.
 //  * The smoothed rows land in shared memory (VB, ROWS rows per chunk); the
-//    output pixels' raw scale*cos / scale*sin go to a small ring (RAW).
+//    output pixels' raw cos / sin go to a small ring (RAW).
 //  * H phase — 4 lanes per row (one per image) stream the chunk's rows with
 //    the same recurrence, multiply by the output pixel's raw phasor and write
 //    the 4 products back in place.
@@ -340,9 +340,9 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
             float* rp = RAW + slot * RAWP + 2 * (q - HALO);
             if (out_col) {
               if (IMGS == 4) {
-                *reinterpret_cast<float2*>(rp) = make_float2(scale * cv, scale * sv);
+                *reinterpret_cast<float2*>(rp) = make_float2(cv, sv);
               } else {
-                rp[pair] = scale * cv;
+                rp[pair] = cv;
               }
             }
           }
@@ -449,8 +449,9 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
         for (; vv < vhi;) {
           if (j < xlim) {
             const float4 pv = *reinterpret_cast<const float4*>(VB + vv * VBP + 4 * (HALO + j));
-            const float num = (IMGS == 4) ? pv.x + pv.y : pv.x + pv.z;
-            const float den = (IMGS == 4) ? pv.z + pv.w : pv.y + pv.w;
+            // the term weight is applied once per output pixel here
+            const float num = scale * ((IMGS == 4) ? pv.x + pv.y : pv.x + pv.z);
+            const float den = scale * ((IMGS == 4) ? pv.z + pv.w : pv.y + pv.w);
             float2* dst = ndrow + (int64_t)vv * p.W + j;
             asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dst), "f"(num), "f"(den));
           }
