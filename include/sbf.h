@@ -187,6 +187,14 @@ int sbf_divide_with_fallback(const double* num, const double* den,
                              const double* fallback, int64_t n, double* out,
                              unsigned long long* count_dev, void* stream);
 
+/* ---- PGM payload codecs (pgmio.py:81-137) ---- */
+/* P5 payload bytes (8-bit or big-endian 16-bit) -> fp32 samples. */
+int sbf_pgm_decode(const void* payload_dev, int bytes_per_sample, int64_t n, float* out_dev,
+                   void* stream);
+/* clamp to [0, maxval], floor(x + 0.5), 8-bit or big-endian 16-bit bytes. */
+int sbf_pgm_encode(const void* img_dev, int dtype, int64_t n, int maxval, void* out_dev,
+                   void* stream);
+
 /* ---- introspection / benchmarking hooks ---- */
 int sbf_num_specialisations(void);
 int sbf_specialisation(int i, int* r, int* passes, int* mode);

@@ -97,6 +97,17 @@ def shiftable_bf(img, params: FilterParams) -> ShiftableResult:
     folded frequency, then num/den with the non-positive-normaliser
     fallback (RuntimeWarning + count).
     """
+    s = stage(img)
+    out, plan, fallbacks = _filter_staged(s, params, out_f64=(s.host or s.dtype == _lib.SBF_F64))
+    if fallbacks:
+        warnings.warn(f"{fallbacks} pixel(s) had a non-positive normalizer; input values kept",
+                      RuntimeWarning, stacklevel=2)
+    result = out.cpu().numpy() if s.host else out
+    return ShiftableResult(result, plan, fallbacks)
+
+
+def _filter_staged(s, params: FilterParams, out_f64: bool):
+    """K1..K4 on a staged device image; returns (device output, KernelPlan, fallbacks)."""
     import torch
 
     if params.family is KernelFamily.POLYNOMIAL:
@@ -105,7 +116,6 @@ def shiftable_bf(img, params: FilterParams) -> ShiftableResult:
     mode = params.resolved_spatial()
     sp = to_c_spatial(mode)
     radius = params.resolved_radius()
-    s = stage(img)
     dev = s.tensor.device
     H, W = s.H, s.W
     use_fixed = params.fixed_T is not None
@@ -123,9 +133,8 @@ def shiftable_bf(img, params: FilterParams) -> ShiftableResult:
         float(params.sigma_r), float(params.epsilon), _lib.RULES.get(params.truncation, -1),
         log_2_over_eps(params.epsilon), plan_dev.data_ptr(), terms.data_ptr(), TERMS_CAP,
         stream), "plan")
-    out_dtype = _lib.SBF_F64 if (s.host or s.dtype == _lib.SBF_F64) else _lib.SBF_F32
-    out = torch.empty((H, W), dtype=torch.float64 if out_dtype == _lib.SBF_F64 else torch.float32,
-                      device=dev)
+    out_dtype = _lib.SBF_F64 if out_f64 else _lib.SBF_F32
+    out = torch.empty((H, W), dtype=torch.float64 if out_f64 else torch.float32, device=dev)
     fb = torch.zeros(1, dtype=torch.int64, device=dev)
     ws_bytes = lib.sbf_filter_workspace(H, W, H, s.dtype, sp, prec)
     ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dev)
@@ -139,16 +148,9 @@ def shiftable_bf(img, params: FilterParams) -> ShiftableResult:
     if plan_c.flags & _lib.PLAN_N_AMBIGUOUS:
         n_host = order_threshold(plan_c.T, params.sigma_r)
         if n_host != plan_c.N:
-            # libm pow() and q*q straddle an integer: redo with the host plan
-            plan_h = select_plan(plan_c.T, params.sigma_r, params.epsilon,
-                                 truncation=params.truncation)
-            return _rerun_with_plan(s, params, plan_h, sp, prec, stats)
-    if fallbacks:
-        warnings.warn(f"{fallbacks} pixel(s) had a non-positive normalizer; input values kept",
-                      RuntimeWarning, stacklevel=2)
-    result = out.cpu().numpy() if s.host else out
-    return ShiftableResult(result, _plan_from_struct(plan_c), fallbacks)
-
-
-def _rerun_with_plan(s, params, plan_h, sp, prec, stats):
-    raise NotImplementedError("ambiguous order threshold; host re-plan not wired yet")
+            # libm pow() and q*q straddle an integer: the device flagged it;
+            # the host twin (libm pow, bit-equal to CPython) is authoritative
+            raise InvalidParameterError(
+                f"order threshold ambiguous at T={plan_c.T!r}: device N={plan_c.N}, "
+                f"libm N={n_host}; pass fixed_T to disambiguate")
+    return out, _plan_from_struct(plan_c), fallbacks
