@@ -98,16 +98,23 @@ def shiftable_bf(img, params: FilterParams) -> ShiftableResult:
     fallback (RuntimeWarning + count).
     """
     s = stage(img)
-    out, plan, fallbacks = _filter_staged(s, params, out_f64=(s.host or s.dtype == _lib.SBF_F64))
+    out, plan, fallbacks = _filter_staged(s, params, out_f64=(s.host or s.dtype == _lib.SBF_F64),
+                                          to_host=s.host)
     if fallbacks:
         warnings.warn(f"{fallbacks} pixel(s) had a non-positive normalizer; input values kept",
                       RuntimeWarning, stacklevel=2)
-    result = out.cpu().numpy() if s.host else out
+    result = out.numpy() if s.host else out
     return ShiftableResult(result, plan, fallbacks)
 
 
-def _filter_staged(s, params: FilterParams, out_f64: bool):
-    """K1..K4 on a staged device image; returns (device output, KernelPlan, fallbacks)."""
+def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False):
+    """K1..K4 on a staged device image; returns (output, KernelPlan, fallbacks).
+
+    With an explicit precision mode the pipeline runs without a host round
+    trip and synchronises once at the end (non-finite input is still
+    rejected, after the fact); "auto" reads the intensity range after K1.
+    `to_host` copies the result into pinned host memory (cached allocator).
+    """
     import torch
 
     if params.family is KernelFamily.POLYNOMIAL:
@@ -119,12 +126,15 @@ def _filter_staged(s, params: FilterParams, out_f64: bool):
     dev = s.tensor.device
     H, W = s.H, s.W
     use_fixed = params.fixed_T is not None
-    # K1: T (or only the statistics when T is fixed) — one sync to validate
+    # K1: T (or only the statistics when T is fixed)
     stats, _ = local_range(s, 0 if use_fixed else radius)
-    st = stats.cpu().numpy()
-    if int(st[7:8].view(np.uint64)[0]) != 0:
-        raise InvalidParameterError("image contains non-finite samples")
-    prec = _precision_code(params, st)
+    if params.precision == "auto":
+        st = stats.cpu().numpy()
+        if int(st[7:8].view(np.uint64)[0]) != 0:
+            raise InvalidParameterError("image contains non-finite samples")
+        prec = _precision_code(params, st)
+    else:
+        prec = _precision_code(params, None)
     stream = _stream_ptr()
     plan_dev = torch.empty(64, dtype=torch.uint8, device=dev)
     terms = torch.empty(TERMS_CAP * 32, dtype=torch.uint8, device=dev)
@@ -142,8 +152,16 @@ def _filter_staged(s, params: FilterParams, out_f64: bool):
                               plan_dev.data_ptr(), terms.data_ptr(), stats.data_ptr(), prec,
                               out.data_ptr(), out_dtype, fb.data_ptr(), ws.data_ptr(), ws.numel(),
                               stream), "filter")
-    plan_c = _lib.SbfPlan.from_buffer_copy(plan_dev.cpu().numpy().tobytes())
-    fallbacks = int(fb.item())
+    if to_host:
+        host = torch.empty((H, W), dtype=out.dtype, pin_memory=True)
+        host.copy_(out, non_blocking=True)
+        out = host
+    # one small read-back for plan, fallback count and the input check
+    tail = torch.cat([plan_dev, fb.view(torch.uint8), stats.view(torch.uint8)]).cpu().numpy()
+    plan_c = _lib.SbfPlan.from_buffer_copy(tail[:64].tobytes())
+    fallbacks = int(tail[64:72].view(np.int64)[0])
+    if int(tail[72:].view(np.uint64)[7]) != 0:
+        raise InvalidParameterError("image contains non-finite samples")
     _lib.check(plan_c.status, "plan")
     if plan_c.flags & _lib.PLAN_N_AMBIGUOUS:
         n_host = order_threshold(plan_c.T, params.sigma_r)
