@@ -306,16 +306,17 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
       const int rs0 = ((t0 - HALO) % RING + RING) % RING;  // RAW slot of step t0
 
       // ===================== V phase =====================
-      // block variants: KIND 0 main (no guards, no border), 1 guarded
-      // (partial block / band edges), 2 border (guarded + renormalisation)
+      // block variants: KIND 0 main (no checks), 1 partial (a full-interior
+      // block cut by a chunk boundary: only the step range is checked),
+      // 2 general (band edges: every condition checked, border renormalised)
       auto vblock = [&](auto kind_tag, const int base) {
         constexpr int KIND = decltype(kind_tag)::value;
-        constexpr bool GUARD = KIND >= 1, BORDER = KIND == 2;
+        constexpr bool GUARD = KIND == 2, BORDER = KIND == 2;
         const float* fb = fcol + (int64_t)(base + L) * p.ld;
         static_for<L>([&](auto jc) {
           constexpr int J = decltype(jc)::value;
           const int t = base + J;
-          if (GUARD && (t < t0 || t >= t1)) return;
+          if (KIND >= 1 && (unsigned)(t - t0) >= (unsigned)(t1 - t0)) return;
           cp_async_wait<L - 1>();
           const float fc = fr[J] - centerf;
           // phasor of this pixel for the current term
@@ -376,12 +377,12 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
         });
       };
       for (int base = (t0 / L) * L; base < t1; base += L) {
-        const bool full = base >= t0 && base + L <= t1 && base >= 2 * HALO &&
-                          base + L <= HALO + Bn && base + 2 * L - 1 <= sf_hi;
-        const bool gin = base - (PASSES + 2) * D - 1 >= sg_lo && base + L - 1 <= sg_hi;
-        if (full && gin)
+        const bool clean = base >= 2 * HALO && base + L <= HALO + Bn &&
+                           base + 2 * L - 1 <= sf_hi &&
+                           base - (PASSES + 2) * D - 1 >= sg_lo && base + L - 1 <= sg_hi;
+        if (clean && base >= t0 && base + L <= t1)
           vblock(std::integral_constant<int, 0>{}, base);
-        else if (gin)
+        else if (clean)
           vblock(std::integral_constant<int, 1>{}, base);
         else
           vblock(std::integral_constant<int, 2>{}, base);
