@@ -141,6 +141,13 @@ int sbf_plan_device(const double* T_dev, int use_fixed, double fixed_T,
                     double log_2_over_eps, sbf_plan* plan_dev,
                     sbf_term* terms_dev, int terms_cap, void* stream);
 
+/* Same with (N, M) resolved on the host (sbf_select_plan, libm pow); for the
+ * rare inputs the device flags SBF_PLAN_N_AMBIGUOUS. */
+int sbf_plan_device_forced(const double* T_dev, int use_fixed, double fixed_T,
+                           double sigma_r, double epsilon, int rule,
+                           double log_2_over_eps, int N, int M, sbf_plan* plan_dev,
+                           sbf_term* terms_dev, int terms_cap, void* stream);
+
 /* Workspace (bytes) for sbf_filter on an H x W buffer producing rows_out rows. */
 size_t sbf_filter_workspace(int64_t H, int64_t W, int64_t rows_out, int dtype,
                             const sbf_spatial* sp, int precision);

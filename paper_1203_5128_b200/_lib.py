@@ -62,6 +62,8 @@ _SIGS = {
     "sbf_local_range": (_int, [_vp, _int, _i64, _i64, _i64, _int, _i64, _i64, _vp, _vp, _vp,
                                C.c_size_t, _vp]),
     "sbf_plan_device": (_int, [_vp, _int, _dbl, _dbl, _dbl, _int, _dbl, _vp, _vp, _int, _vp]),
+    "sbf_plan_device_forced": (_int, [_vp, _int, _dbl, _dbl, _dbl, _int, _dbl, _int, _int, _vp, _vp,
+                                      _int, _vp]),
     "sbf_filter_workspace": (C.c_size_t, [_i64, _i64, _i64, _int, C.POINTER(SbfSpatial), _int]),
     "sbf_filter": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _i64, _i64,
                           C.POINTER(SbfSpatial), _vp, _vp, _vp, _int, _vp, _int, _vp, _vp,

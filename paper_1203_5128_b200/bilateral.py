@@ -138,11 +138,19 @@ def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False
     stream = _stream_ptr()
     plan_dev = torch.empty(64, dtype=torch.uint8, device=dev)
     terms = torch.empty(TERMS_CAP * 32, dtype=torch.uint8, device=dev)
-    _lib.check(lib.sbf_plan_device(
-        stats.data_ptr(), 1 if use_fixed else 0, float(params.fixed_T) if use_fixed else 0.0,
-        float(params.sigma_r), float(params.epsilon), _lib.RULES.get(params.truncation, -1),
-        log_2_over_eps(params.epsilon), plan_dev.data_ptr(), terms.data_ptr(), TERMS_CAP,
-        stream), "plan")
+    def plan_on_device(forced=None):
+        args = (stats.data_ptr(), 1 if use_fixed else 0,
+                float(params.fixed_T) if use_fixed else 0.0, float(params.sigma_r),
+                float(params.epsilon), _lib.RULES.get(params.truncation, -1),
+                log_2_over_eps(params.epsilon))
+        if forced is None:
+            _lib.check(lib.sbf_plan_device(*args, plan_dev.data_ptr(), terms.data_ptr(),
+                                           TERMS_CAP, stream), "plan")
+        else:
+            _lib.check(lib.sbf_plan_device_forced(*args, forced[0], forced[1], plan_dev.data_ptr(),
+                                                  terms.data_ptr(), TERMS_CAP, stream), "plan")
+
+    plan_on_device()
     out_dtype = _lib.SBF_F64 if out_f64 else _lib.SBF_F32
     out = torch.empty((H, W), dtype=torch.float64 if out_f64 else torch.float32, device=dev)
     fb = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -152,6 +160,7 @@ def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False
                               plan_dev.data_ptr(), terms.data_ptr(), stats.data_ptr(), prec,
                               out.data_ptr(), out_dtype, fb.data_ptr(), ws.data_ptr(), ws.numel(),
                               stream), "filter")
+    out_dev = out
     if to_host:
         host = torch.empty((H, W), dtype=out.dtype, pin_memory=True)
         host.copy_(out, non_blocking=True)
@@ -164,11 +173,18 @@ def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False
         raise InvalidParameterError("image contains non-finite samples")
     _lib.check(plan_c.status, "plan")
     if plan_c.flags & _lib.PLAN_N_AMBIGUOUS:
-        n_host = order_threshold(plan_c.T, params.sigma_r)
-        if n_host != plan_c.N:
-            # libm pow() and q*q straddle an integer: the device flagged it;
-            # the host twin (libm pow, bit-equal to CPython) is authoritative
-            raise InvalidParameterError(
-                f"order threshold ambiguous at T={plan_c.T!r}: device N={plan_c.N}, "
-                f"libm N={n_host}; pass fixed_T to disambiguate")
+        # ceil(0.405 q^2) straddles an integer within 2 ulp of q^2: the host twin
+        # (libm pow, bit-equal to CPython) decides, and the filter is re-run
+        ph = select_plan(plan_c.T, params.sigma_r, params.epsilon, truncation=params.truncation)
+        if (ph.N, ph.M) != (plan_c.N, plan_c.M):
+            plan_on_device(forced=(ph.N, ph.M))
+            fb.zero_()
+            _lib.check(lib.sbf_filter(s.tensor.data_ptr(), s.dtype, H, W, W, 0, H, 0, H, sp,
+                                      plan_dev.data_ptr(), terms.data_ptr(), stats.data_ptr(),
+                                      prec, out_dev.data_ptr(), out_dtype, fb.data_ptr(),
+                                      ws.data_ptr(), ws.numel(), stream), "filter")
+            if to_host:
+                out.copy_(out_dev)
+            plan_c = _lib.SbfPlan.from_buffer_copy(plan_dev.cpu().numpy().tobytes())
+            fallbacks = int(fb.item())
     return out, _plan_from_struct(plan_c), fallbacks

@@ -367,6 +367,16 @@ int sbf_plan_device(const double* T_dev, int use_fixed, double fixed_T, double s
                           plan_dev, terms_dev, terms_cap, as_stream(stream));
 }
 
+// Same as sbf_plan_device with (N, M) resolved on the host (libm pow); used
+// only when the device plan came back flagged SBF_PLAN_N_AMBIGUOUS.
+int sbf_plan_device_forced(const double* T_dev, int use_fixed, double fixed_T, double sigma_r,
+                           double epsilon, int rule, double log_2_over_eps, int N, int M,
+                           sbf_plan* plan_dev, sbf_term* terms_dev, int terms_cap, void* stream) {
+  SBF_REQUIRE(sigma_r > 0.0 && N >= 1 && M >= 0 && 2 * M < N, SBF_ERR_INVALID, "bad forced plan");
+  return sbf::launch_plan(T_dev, use_fixed, fixed_T, sigma_r, epsilon, rule, log_2_over_eps,
+                          plan_dev, terms_dev, terms_cap, as_stream(stream), N, M);
+}
+
 size_t sbf_filter_workspace(int64_t H, int64_t W, int64_t rows_out, int dtype,
                             const sbf_spatial* sp, int precision) {
   if (!sp) return 0;

@@ -82,7 +82,7 @@ size_t local_range_ws(int64_t H, int64_t W, int dtype);
 
 int launch_plan(const double* T_dev, int use_fixed, double fixed_T, double sigma_r, double eps,
                 int rule, double log_2_over_eps, sbf_plan* plan_dev, sbf_term* terms_dev,
-                int terms_cap, cudaStream_t st);
+                int terms_cap, cudaStream_t st, int forced_N = 0, int forced_M = 0);
 
 struct FilterLaunch {
   const void* f;

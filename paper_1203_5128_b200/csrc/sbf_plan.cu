@@ -18,11 +18,21 @@ namespace {
 __global__ void plan_kernel(const double* __restrict__ T_dev, int use_fixed, double fixed_T,
                             double sigma_r, double eps, int rule, double log_2_over_eps,
                             sbf_plan* __restrict__ plan_out, sbf_term* __restrict__ terms,
-                            int cap) {
+                            int cap, int forced_N, int forced_M) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const double T = use_fixed ? fixed_T : T_dev[0];
   sbf_plan p;
   select_plan(T, sigma_r, eps, rule, log_2_over_eps, &p);
+  if (forced_N > 0 && p.status == SBF_OK) {
+    // host-resolved (N, M) (libm pow, bit-equal to CPython) after the device
+    // flagged SBF_PLAN_N_AMBIGUOUS; the term table follows from it
+    p.N = forced_N;
+    p.M = forced_M;
+    p.K = forced_N / 2 - forced_M + 1;
+    p.K_eval = p.K;
+    p.gamma = 1.0 / (sqrt((double)forced_N) * sigma_r);
+    p.flags &= ~SBF_PLAN_N_AMBIGUOUS;
+  }
   if (p.status == SBF_OK) {
     const int N = p.N, M = p.M, nc = N / 2;
     // total = sum_{n=0}^{N} C(N,n)/C(N,nc) by symmetry from the half sum
@@ -66,11 +76,11 @@ __global__ void plan_kernel(const double* __restrict__ T_dev, int use_fixed, dou
 
 int launch_plan(const double* T_dev, int use_fixed, double fixed_T, double sigma_r, double eps,
                 int rule, double log_2_over_eps, sbf_plan* plan_dev, sbf_term* terms_dev,
-                int terms_cap, cudaStream_t st) {
+                int terms_cap, cudaStream_t st, int forced_N, int forced_M) {
   SBF_REQUIRE(plan_dev && terms_dev && terms_cap > 0, SBF_ERR_INVALID, "null plan/terms buffer");
   SBF_REQUIRE(use_fixed || T_dev, SBF_ERR_INVALID, "null T");
   plan_kernel<<<1, 32, 0, st>>>(T_dev, use_fixed, fixed_T, sigma_r, eps, rule, log_2_over_eps,
-                                plan_dev, terms_dev, terms_cap);
+                                plan_dev, terms_dev, terms_cap, forced_N, forced_M);
   SBF_CHECK_LAUNCH();
   return SBF_OK;
 }

@@ -43,7 +43,9 @@ SBF_HD inline int order_threshold(double T, double sigma_r, int* flags, int* sta
   double hi = kOrderCoeff * next_up(next_up(q2));
   if (ceil(lo) != ceil(hi)) *flags |= SBF_PLAN_N_AMBIGUOUS;
 #else
-  double q2 = pow(q, 2.0);
+  // a runtime exponent: compilers fold pow(q, 2.0) into q*q, CPython does not
+  volatile double two = 2.0;
+  double q2 = pow(q, two);
 #endif
   double x = kOrderCoeff * q2;
   if (!(x <= kMaxOrder)) {

@@ -181,3 +181,13 @@ def test_strip_filter_emulated_ranks_match_full_image():
         pl = f.plans_host()[0]
         assert (pl.N, pl.M) == (full.plan.N, full.plan.M)
     assert_close_image(gather_strips(outs, strips), full.image, 2e-3, 2e-4)
+
+
+def test_ambiguous_order_threshold_replanned_on_host():
+    """Device q*q gives N=3707, CPython's libm pow gives 3706: the device flags
+    the ambiguity and the wrapper re-plans with the host twin."""
+    T = 95.65885888902615
+    img = np.random.default_rng(4).uniform(0, 50, (12, 12))
+    res = P.shiftable_bf(img, P.FilterParams(sigma_s=1.0, sigma_r=1.0, epsilon=0.2, fixed_T=T))
+    ref = O.shiftable_bf(img, 1.0, 1.0, 0.2, fixed_T=T)
+    assert (res.plan.N, res.plan.M) == (ref["N"], ref["M"]) == (3706, ref["M"])

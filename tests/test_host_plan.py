@@ -102,3 +102,10 @@ def test_expansion_matches_reference_golden():
     e = P.raised_cosine_expansion(plan)
     np.testing.assert_array_equal(e.weights, g["w_229_79"])
     np.testing.assert_array_equal(e.frequencies, g["f_229_79"])
+
+
+def test_libm_pow_ambiguity_resolved_like_cpython():
+    # (T/sigma_r)**2 via libm pow differs from q*q here and moves the ceiling
+    T = 95.65885888902615
+    assert O.order_threshold(T, 1.0) == 3706
+    assert P.order_threshold(T, 1.0) == 3706        # host twin calls pow() like CPython
