@@ -191,3 +191,36 @@ def test_ambiguous_order_threshold_replanned_on_host():
     res = P.shiftable_bf(img, P.FilterParams(sigma_s=1.0, sigma_r=1.0, epsilon=0.2, fixed_T=T))
     ref = O.shiftable_bf(img, 1.0, 1.0, 0.2, fixed_T=T)
     assert (res.plan.N, res.plan.M) == (ref["N"], ref["M"]) == (3706, ref["M"])
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 7), (7, 1), (3, 3), (2, 300), (300, 2), (5, 129), (129, 6)])
+def test_degenerate_shapes_vs_oracle(shape):
+    img = np.random.default_rng(sum(shape)).uniform(0, 255, shape)
+    for sp, oracle_sp in ((None, None), (P.Box(2), ("box", 2)), (P.Box(0), ("box", 0))):
+        params = P.FilterParams(sigma_s=2.0, sigma_r=25.0, epsilon=0.01, spatial=sp)
+        res = P.shiftable_bf(img, params)
+        ref = O.shiftable_bf(img, 2.0, 25.0, 0.01, spatial=oracle_sp)
+        assert (res.plan.T, res.plan.N, res.plan.M) == (ref["T"], ref["N"], ref["M"])
+        assert_close_image(res.image, ref["image"])
+
+
+@pytest.mark.parametrize("sigma_s,passes", [(2.5, 1), (4.0, 2), (10.0, 4), (20.0, 3)])
+def test_generic_spatial_paths_vs_oracle(sigma_s, passes):
+    """Pass counts / radii without a specialised K3 (fp64 generic path)."""
+    img = np.random.default_rng(7).uniform(0, 255, (70, 90))
+    params = P.FilterParams(sigma_s=sigma_s, sigma_r=30.0, epsilon=0.01,
+                            spatial=P.IteratedBox(sigma_s, passes))
+    res = P.shiftable_bf(img, params)
+    ref = O.shiftable_bf(img, sigma_s, 30.0, 0.01, spatial=("iterated", sigma_s, passes))
+    assert (res.plan.N, res.plan.M) == (ref["N"], ref["M"])
+    assert_close_image(res.image, ref["image"])
+
+
+def test_torch_cuda_tensor_in_and_out():
+    import torch
+    img = config_image(2, size=128)
+    t = torch.from_numpy(img).cuda()
+    res = P.shiftable_bf(t, P.FilterParams(sigma_s=5, sigma_r=10, epsilon=0.01))
+    assert res.image.is_cuda and res.image.dtype == torch.float32
+    ref = O.shiftable_bf(img, 5.0, 10.0, 0.01)
+    assert_close_image(res.image.cpu().numpy(), ref["image"])
