@@ -65,20 +65,29 @@ def _compile(args):
     return obj, p.returncode, p.stdout + p.stderr
 
 
-def build(kind: str = "full", jobs: int | None = None, verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(kind: str = "full", jobs: int | None = None, verbose: bool = False,
+          variant: str | None = None, defs: list[str] | None = None) -> str:
+    """Compile and link.  `variant` + `defs` build an experimental copy
+    (extra -D flags on every object) into _build_<variant>/libsbf_<variant>.so,
+    loadable with SBF_LIB=...; the default library is untouched."""
+    obj_dir, lib = OBJ, LIB
+    defs = list(defs or [])
+    if variant:
+        obj_dir = OBJ + "_" + variant
+        lib = os.path.join(HERE, f"libsbf_{variant}.so")
+    os.makedirs(obj_dir, exist_ok=True)
     inst = instantiations(kind)
     inc = os.path.join(CSRC, "sbf_terms_list.inc")
     text = "".join(f"SBF_X({r}, {p}, {m})\n" for r, p, m in inst)
     if not os.path.exists(inc) or open(inc).read() != text:
         with open(inc, "w") as fh:
             fh.write(text)
-    jobs_list = [(os.path.join(CSRC, s), os.path.join(OBJ, s.replace(".cu", ".o")), [])
+    jobs_list = [(os.path.join(CSRC, s), os.path.join(obj_dir, s.replace(".cu", ".o")), defs)
                  for s in SOURCES]
     for r, p, m in inst:
         jobs_list.append((os.path.join(CSRC, "sbf_terms_inst.cu"),
-                          os.path.join(OBJ, f"terms_r{r}_p{p}_m{m}.o"),
-                          [f"-DSBF_R={r}", f"-DSBF_P={p}", f"-DSBF_M={m}"]))
+                          os.path.join(obj_dir, f"terms_r{r}_p{p}_m{m}.o"),
+                          defs + [f"-DSBF_R={r}", f"-DSBF_P={p}", f"-DSBF_M={m}"]))
     jobs = jobs or max(1, os.cpu_count() or 1)
     failed = []
     with cf.ThreadPoolExecutor(jobs) as ex:
@@ -92,12 +101,12 @@ def build(kind: str = "full", jobs: int | None = None, verbose: bool = False) ->
             sys.stderr.write(f"--- {obj}\n{out}\n")
         raise RuntimeError(f"nvcc failed for {len(failed)} object(s)")
     objs = [j[1] for j in jobs_list]
-    if not _newer(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
+    if not _newer(lib, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-lcudart"]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError("link failed:\n" + p.stdout + p.stderr)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
@@ -107,5 +116,7 @@ if __name__ == "__main__":
     g.add_argument("--min", action="store_true")
     ap.add_argument("-j", type=int, default=None)
     ap.add_argument("-v", action="store_true")
+    ap.add_argument("--variant", default=None, help="experimental build tag")
+    ap.add_argument("-D", dest="defs", action="append", default=[], help="extra macro (NAME=VALUE)")
     a = ap.parse_args()
-    print(build("min" if a.min else "full", a.j, a.v))
+    print(build("min" if a.min else "full", a.j, a.v, a.variant, ["-D" + d for d in a.defs]))
