@@ -95,3 +95,43 @@ def test_config1_plan_and_crop():
     assert O.compute_T(img, 9) == 251.39522633396712
     assert O.select_plan(251.39522633396712, 30.0, 0.01) == (251.39522633396712, 29, 7)
     np.testing.assert_array_equal(O.max_filter_2d(img, 9)[::8, ::8], g["M"])
+
+
+# ---- the C restatement (oracle/sbf_oracle.c), pinned to the same vectors ----
+def _coracle():
+    from oracle import coracle
+    coracle.build()
+    return coracle
+
+
+def test_c_oracle_max_filter_bit_exact():
+    CO = _coracle()
+    g = golden("maxfilter.npz")
+    for k in range(40):
+        img, R = g[f"img_{k}"], int(g[f"R_{k}"])
+        assert np.array_equal(CO.max_filter_2d(img, R), g[f"M_{k}"])
+        assert CO.compute_T(img, R) == float(g[f"T_{k}"])
+
+
+@pytest.mark.parametrize("k", range(16))
+def test_c_oracle_matches_reference(k):
+    CO = _coracle()
+    g = golden("bf_small.npz")
+    ss, sr, eps, boxr, fT, tr = g[f"par_{k}"]
+    spatial = None if boxr < 0 else ("box", int(boxr))
+    res = CO.shiftable_bf(g[f"img_{k}"], float(ss), float(sr), float(eps), spatial=spatial,
+                          fixed_T=None if math.isnan(fT) else float(fT), truncation=RULES[int(tr)])
+    T, N, M, fb = g[f"plan_{k}"]
+    assert (res["T"], res["N"], res["M"], res["fallback_pixels"]) == (T, int(N), int(M), int(fb))
+    np.testing.assert_allclose(res["image"], g[f"out_{k}"], rtol=1e-9, atol=1e-7)
+
+
+def test_c_oracle_agrees_with_numpy_oracle():
+    CO = _coracle()
+    rng = np.random.default_rng(5)
+    for spatial in (None, ("box", 3), ("iterated", 2.5, 2)):
+        img = rng.uniform(0, 255, (41, 67))
+        a = CO.shiftable_bf(img, 2.5, 20.0, 0.01, spatial=spatial)
+        b = O.shiftable_bf(img, 2.5, 20.0, 0.01, spatial=spatial)
+        assert (a["T"], a["N"], a["M"]) == (b["T"], b["N"], b["M"])
+        np.testing.assert_allclose(a["image"], b["image"], rtol=1e-10, atol=1e-9)
