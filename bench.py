@@ -101,15 +101,20 @@ class ClockSampler:
 # ----------------------------------------------------------------------------
 # CPU baseline (the oracle port; reference-arm and cpu_baseline leg only)
 # ----------------------------------------------------------------------------
-def _cpu_band(args):
-    img, y0, y1, halo, T, p = args
+def _cpu_init(barrier):
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     from oracle import coracle as CO
-    a, b = max(0, y0 - halo), min(img.shape[0], y1 + halo)
+    CO.load()
+    barrier.wait()  # every worker is up and has its library loaded
+
+
+def _cpu_band(args):
+    part, rows_out, T, p = args  # part = output rows plus their halo
+    from oracle import coracle as CO
     t = time.perf_counter()
-    out = CO.shiftable_bf(img[a:b], p["sigma_s"], p["sigma_r"], p["epsilon"], fixed_T=T)
+    out = CO.shiftable_bf(part, p["sigma_s"], p["sigma_r"], p["epsilon"], fixed_T=T)
     dt = time.perf_counter() - t
-    return (y1 - y0) * img.shape[1], dt, out["N"], out["M"]
+    return rows_out * part.shape[1], dt, out["N"], out["M"]
 
 
 def cpu_baseline(cfg=2, min_band_rows=32, max_procs=None):
@@ -133,12 +138,20 @@ def cpu_baseline(cfg=2, min_band_rows=32, max_procs=None):
     H = min(img.shape[0], max(min_band_rows, int(8e6) // img.shape[1]))
     procs = max(1, min(max_procs or os.cpu_count() or 1, H // min_band_rows))
     band_rows = -(-H // procs)
-    jobs = [(img, k * band_rows, min(H, (k + 1) * band_rows), halo, T, p) for k in range(procs)
-            if k * band_rows < H]
-    t = time.perf_counter()
-    with mp.get_context("fork").Pool(procs) as pool:
-        res = pool.map(_cpu_band, jobs)
-    wall = time.perf_counter() - t
+    jobs = []
+    for y0 in range(0, H, band_rows):
+        y1 = min(H, y0 + band_rows)
+        a, b = max(0, y0 - halo), min(img.shape[0], y1 + halo)
+        jobs.append((img[a:b], y1 - y0, T, p))
+    # spawn (the caller holds CUDA threads); workers are started and warmed
+    # before the clock starts, then one band per worker is timed
+    ctx = mp.get_context("spawn")
+    barrier = ctx.Barrier(len(jobs) + 1)
+    with ctx.Pool(len(jobs), initializer=_cpu_init, initargs=(barrier,)) as pool:
+        barrier.wait()
+        t = time.perf_counter()
+        res = pool.map(_cpu_band, jobs, chunksize=1)
+        wall = time.perf_counter() - t
     px = sum(x[0] for x in res)
     what = "whole image" if H == img.shape[0] else f"first {H} rows"
     sample = (f"C oracle (oracle/sbf_oracle.c, float64), {what}: {len(jobs)} bands x "

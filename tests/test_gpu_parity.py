@@ -224,3 +224,17 @@ def test_torch_cuda_tensor_in_and_out():
     assert res.image.is_cuda and res.image.dtype == torch.float32
     ref = O.shiftable_bf(img, 5.0, 10.0, 0.01)
     assert_close_image(res.image.cpu().numpy(), ref["image"])
+
+
+@pytest.mark.parametrize("cfg,size,idx", [(2, None, 0), (4, None, 0), (5, 4096, 0), (3, None, 0)])
+def test_config_full_size_vs_c_oracle(cfg, size, idx):
+    """Full BASELINE sizes (config 5 at 4096^2) against the band-parallel C oracle."""
+    import _oracle_par
+    c = {2: (5.0, 10.0), 3: (8.0, 800.0), 4: (6.0, 20.0), 5: (12.0, 15.0)}[cfg]
+    img = config_image(cfg, idx, size=size)
+    res = P.shiftable_bf(img, P.FilterParams(sigma_s=c[0], sigma_r=c[1], epsilon=0.01))
+    ref = _oracle_par.shiftable_bf_full(img, c[0], c[1], 0.01)
+    assert (res.plan.T, res.plan.N, res.plan.M) == (ref["T"], ref["N"], ref["M"])
+    scale = max(1.0, float(np.abs(img).max()) / 255.0)
+    mx, rms = assert_close_image(res.image, ref["image"], MAX_ABS * scale, RMS * scale)
+    print(f"cfg{cfg} {img.shape}: max {mx:.3g} rms {rms:.3g} (scale {scale:.3g})")

@@ -135,3 +135,16 @@ def test_c_oracle_agrees_with_numpy_oracle():
         b = O.shiftable_bf(img, 2.5, 20.0, 0.01, spatial=spatial)
         assert (a["T"], a["N"], a["M"]) == (b["T"], b["N"], b["M"])
         np.testing.assert_allclose(a["image"], b["image"], rtol=1e-10, atol=1e-9)
+
+
+def test_band_split_is_exact():
+    """The band-parallel helper used by the full-size GPU parity tests
+    reproduces the whole-image oracle."""
+    import _oracle_par
+    CO = _coracle()
+    from paper_1203_5128_b200.workloads import config_image
+    img = config_image(2, size=160)
+    whole = CO.shiftable_bf(img, 5.0, 10.0, 0.01)
+    split = _oracle_par.shiftable_bf_full(img, 5.0, 10.0, 0.01, procs=4)
+    assert (split["T"], split["N"], split["M"]) == (whole["T"], whole["N"], whole["M"])
+    np.testing.assert_allclose(split["image"], whole["image"], rtol=0, atol=1e-9)
