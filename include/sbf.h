@@ -202,6 +202,16 @@ int sbf_pgm_decode(const void* payload_dev, int bytes_per_sample, int64_t n, flo
 int sbf_pgm_encode(const void* img_dev, int dtype, int64_t n, int maxval, void* out_dev,
                    void* stream);
 
+/* ---- brute-force bilateral filter (accuracy oracle at full size) ----
+ * Replaces reference bilateral.py:205-239 `direct_bf(img, spatial,
+ * gaussian_range(sigma_r), radius)`: out(x) = sum_y w(y) g(f(y)-f(x)) f(y) /
+ * sum_y w(y) g(...) over the in-bounds (2R+1)^2 window, g Gaussian of width
+ * sigma_r, w(dy,dx) = taps[dy+R] taps[dx+R] (taps == NULL: uniform, the Box
+ * mode; spatial.py:197-213).  R <= 255.  Device buffers, stream-ordered. */
+int sbf_direct_bf(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int R,
+                  const double* taps_host, double sigma_r, void* out, int out_dtype,
+                  void* stream);
+
 /* ---- introspection / benchmarking hooks ---- */
 int sbf_num_specialisations(void);
 int sbf_specialisation(int i, int* r, int* passes, int* mode);

@@ -312,6 +312,42 @@ def shiftable_bf(img, sigma_s, sigma_r, epsilon=0.0, spatial=None,
     return dict(image=out, T=T, N=N, M=M, fallback_pixels=n_bad)
 
 
+def direct_bf(img, spatial, sigma_r, radius=None):
+    """bilateral.py:205-239 with gaussian_range (:88-99) and the window weights
+    of spatial.py:155-157 / 197-213.  `spatial` is ('box', r) or
+    ('fir', sigma_s, r)."""
+    f = as_image(img)
+    if radius is None:
+        radius = spatial[1] if spatial[0] == "box" else spatial[2]
+    R = int(radius)
+    if spatial[0] == "box":
+        taps = np.ones(2 * R + 1)
+    else:
+        k = np.arange(-R, R + 1, dtype=np.float64)
+        taps = np.exp(-(k * k) / (2.0 * spatial[1] * spatial[1]))
+    weights = np.outer(taps, taps)
+    inv = 1.0 / (2.0 * sigma_r * sigma_r)
+    h, w = f.shape
+    num = np.zeros_like(f)
+    den = np.zeros_like(f)
+    for dy in range(-R, R + 1):
+        if abs(dy) >= h:
+            continue
+        ys, yd = slice(max(0, dy), h + min(0, dy)), slice(max(0, -dy), h - max(0, dy))
+        for dx in range(-R, R + 1):
+            wsp = weights[dy + R, dx + R]
+            if wsp == 0.0 or abs(dx) >= w:
+                continue
+            xs, xd = slice(max(0, dx), w + min(0, dx)), slice(max(0, -dx), w - max(0, dx))
+            nb = f[ys, xs]
+            d = nb - f[yd, xd]
+            wr = wsp * np.exp(-(d * d) * inv)
+            num[yd, xd] += wr * nb
+            den[yd, xd] += wr
+    out, _ = divide_with_fallback(num, den, f)
+    return out
+
+
 def metrics(a, b):
     """metrics.py:19-28 — (mse, mse_db, max_abs)."""
     d = as_image(a) - as_image(b)

@@ -1,0 +1,108 @@
+// K5 — brute-force bilateral filter over the clamped window (reference
+// bilateral.py:205-239 `direct_bf` with `gaussian_range`, bilateral.py:88-99,
+// and the window weights of spatial.py:197-213: uniform for Box, the outer
+// product of sampled Gaussian taps for FirGaussian).
+//
+// The accuracy oracle at full sizes: O(R^2) per
+// pixel, so it is an FP32/MUFU-bound kernel, not a hot path.  One thread per
+// output pixel (two rows per thread for ILP); neighbours come straight from
+// global memory (warp-coalesced row segments, L1-resident across dx).  The
+// spatial weight is folded into the exponent in log2 domain:
+//     w_s(dy, dx) exp(-d^2 / (2 sr^2)) = exp2(ly[dy] + lx[dx] - d^2 log2(e) / (2 sr^2))
+// (a zero tap gives -inf, i.e. weight 0, as in the reference).  Only in-bounds
+// neighbours contribute (the reference's offset_slices), num / den in fp32,
+// den <= 0 (impossible with the positive Gaussian) falls back to the input.
+#include "sbf_common.cuh"
+
+namespace sbf {
+namespace {
+
+constexpr int kDirectMaxR = 255;
+
+struct DirectParams {
+  int64_t H, W, ld;
+  int R;
+  float c;                      // -log2(e) / (2 sigma_r^2)
+  float ltap[2 * kDirectMaxR + 1];  // log2 of the 1-D taps
+};
+
+template <typename FT, typename OT>
+__global__ void __launch_bounds__(256) direct_kernel(const FT* __restrict__ f, OT* __restrict__ out,
+                                                     const __grid_constant__ DirectParams p) {
+  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t y0 = ((int64_t)blockIdx.y * blockDim.y + threadIdx.y) * 2;
+  if (x >= p.W || y0 >= p.H) return;
+  const bool two = y0 + 1 < p.H;
+  const int R = p.R;
+  const float c0 = (float)f[y0 * p.ld + x];
+  const float c1 = two ? (float)f[(y0 + 1) * p.ld + x] : c0;
+  const int dx_lo = (int)smax<int64_t>(-R, -x), dx_hi = (int)smin<int64_t>(R, p.W - 1 - x);
+  float n0 = 0.f, d0 = 0.f, n1 = 0.f, d1 = 0.f;
+  // rows y0 + dy for dy in [-R, R + 1]: row s serves output 0 at dy = s and
+  // output 1 at dy = s - 1
+  const int s_lo = (int)smax<int64_t>(-R, -y0), s_hi = (int)smin<int64_t>(R + 1, p.H - 1 - y0);
+  for (int s = s_lo; s <= s_hi; ++s) {
+    const FT* row = f + (y0 + s) * p.ld + x;
+    const bool use0 = s <= R;
+    const bool use1 = two && s - 1 >= -R;
+    const float ly0 = use0 ? p.ltap[s + R] : -INFINITY;
+    const float ly1 = use1 ? p.ltap[s - 1 + R] : -INFINITY;
+#pragma unroll 4
+    for (int dx = dx_lo; dx <= dx_hi; ++dx) {
+      const float v = (float)row[dx];
+      const float lx = p.ltap[dx + R];
+      const float e0 = v - c0, e1 = v - c1;
+      const float w0 = exp2f(fmaf(e0 * e0, p.c, ly0 + lx));
+      const float w1 = exp2f(fmaf(e1 * e1, p.c, ly1 + lx));
+      n0 = fmaf(w0, v, n0);
+      d0 += w0;
+      n1 = fmaf(w1, v, n1);
+      d1 += w1;
+    }
+  }
+  out[y0 * p.W + x] = (OT)(d0 > 0.f ? n0 / d0 : c0);
+  if (two) out[(y0 + 1) * p.W + x] = (OT)(d1 > 0.f ? n1 / d1 : c1);
+}
+
+template <typename FT, typename OT>
+int launch_direct(const void* f, void* out, const DirectParams& p, cudaStream_t st) {
+  dim3 block(32, 8);
+  dim3 grid((unsigned)((p.W + 31) / 32), (unsigned)((p.H + 15) / 16));
+  direct_kernel<FT, OT><<<grid, block, 0, st>>>(static_cast<const FT*>(f), static_cast<OT*>(out), p);
+  SBF_CHECK_LAUNCH();
+  return SBF_OK;
+}
+
+}  // namespace
+}  // namespace sbf
+
+extern "C" int sbf_direct_bf(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int R,
+                             const double* taps, double sigma_r, void* out, int out_dtype,
+                             void* stream) {
+  using namespace sbf;
+  SBF_REQUIRE(f && out, SBF_ERR_INVALID, "null pointer");
+  SBF_REQUIRE(dtype == SBF_F32 || dtype == SBF_F64, SBF_ERR_INVALID, "bad dtype");
+  SBF_REQUIRE(out_dtype == SBF_F32 || out_dtype == SBF_F64, SBF_ERR_INVALID, "bad out dtype");
+  SBF_REQUIRE(H >= 1 && W >= 1 && ld >= W, SBF_ERR_INVALID, "bad image shape");
+  SBF_REQUIRE(R >= 0 && R <= kDirectMaxR, SBF_ERR_UNSUPPORTED, "direct_bf radius %d outside [0, %d]",
+              R, kDirectMaxR);
+  SBF_REQUIRE(sigma_r > 0.0, SBF_ERR_INVALID, "sigma_r must be positive");
+  DirectParams p;
+  memset(&p, 0, sizeof(p));
+  p.H = H;
+  p.W = W;
+  p.ld = ld;
+  p.R = R;
+  p.c = (float)(-1.4426950408889634 / (2.0 * sigma_r * sigma_r));
+  for (int k = 0; k <= 2 * R; ++k) {
+    const double t = taps ? taps[k] : 1.0;
+    SBF_REQUIRE(t >= 0.0 && t == t, SBF_ERR_INVALID, "spatial taps must be non-negative");
+    p.ltap[k] = t > 0.0 ? (float)log2(t) : -INFINITY;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == SBF_F32)
+    return out_dtype == SBF_F32 ? launch_direct<float, float>(f, out, p, st)
+                                : launch_direct<float, double>(f, out, p, st);
+  return out_dtype == SBF_F32 ? launch_direct<double, float>(f, out, p, st)
+                              : launch_direct<double, double>(f, out, p, st);
+}

@@ -62,23 +62,34 @@ struct TermParams {
   int64_t nd_group_stride;  // (num, den) pairs per group
 };
 
+#ifndef SBF_IMGS4_MAX_R
+#define SBF_IMGS4_MAX_R 4  // radii up to this run 4 images per V thread
+#endif
+#ifndef SBF_MAX_ROWS
+#define SBF_MAX_ROWS 64    // rows per chunk cap
+#endif
+#ifndef SBF_IMGS2_2CTA_MAX_R
+#define SBF_IMGS2_2CTA_MAX_R -1  // 2-image layouts up to this radius run 2 CTAs/SM
+#endif
+
 template <int R, int PASSES>
 struct TermCfg {
   static constexpr int D = R + 1;
   static constexpr int L = 2 * R + 3;
   static constexpr int HALO = PASSES * D;
-  static constexpr int IMGS = (R <= 4) ? 4 : 2;
+  static constexpr int IMGS = (R <= SBF_IMGS4_MAX_R) ? 4 : 2;
   static constexpr int HALO_W = 128;
   static constexpr int WC = HALO_W - 2 * HALO;
   static constexpr int NB = (HALO_W + L - 1) / L;  // H-phase blocks per row
   static constexpr int VB_COLS = NB * L;
   static constexpr int VB_PITCH = 4 * (VB_COLS + ((VB_COLS % 2 == 0) ? 1 : 2));  // == 4 mod 8 words
   static constexpr int THREADS = HALO_W * 4 / IMGS;
-  static constexpr int ROWS = THREADS / 4;
+  static constexpr int ROWS_CAP = SBF_MAX_ROWS > HALO ? SBF_MAX_ROWS : HALO;
+  static constexpr int ROWS = THREADS / 4 < ROWS_CAP ? THREADS / 4 : ROWS_CAP;
   static constexpr int RING = ROWS + HALO;
   static constexpr int RAW_PITCH = 2 * WC + 2;  // floats; == 2 mod 4 (WC even)
   static constexpr int GOFF = (PASSES + 2) * D + 2;  // table offset (most negative position)
-  static constexpr int MIN_BLOCKS = (IMGS == 4) ? 2 : 1;
+  static constexpr int MIN_BLOCKS = (IMGS == 4 || R <= SBF_IMGS2_2CTA_MAX_R) ? 2 : 1;
   static_assert(WC > 0, "halo too wide for a 128-column strip");
   static_assert(HALO <= ROWS, "RAW ring assumes halo <= rows per chunk");
 };

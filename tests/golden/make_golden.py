@@ -178,6 +178,35 @@ def config1():
                         M=rm.max_filter_2d(img, 9)[::8, ::8])
 
 
+def direct_cases():
+    """Brute-force direct_bf (bilateral.py:205-239) with gaussian_range."""
+    from shiftbf.bilateral import direct_bf, gaussian_range
+    rng = np.random.default_rng(20260811)
+    cases = [
+        # (h, w, spatial, radius override, sigma_r, lo, hi)
+        (23, 31, ("box", 2), None, 30.0, 0, 255),
+        (40, 37, ("fir", 3.0, 9), None, 20.0, 0, 255),
+        (17, 64, ("fir", 2.0, 6), 4, 50.0, 0, 255),
+        (30, 30, ("box", 5), None, 10.0, 0, 255),
+        (12, 9, ("fir", 5.0, 15), None, 25.0, 0, 255),
+        (36, 28, ("fir", 4.0, 12), None, 800.0, 0, 65535),
+        (1, 50, ("box", 3), None, 30.0, 0, 255),
+        (45, 45, ("fir", 1.5, 5), None, 5.0, 0, 255),
+    ]
+    out = {}
+    for k, (h, w, sp, rad, sr, lo, hi) in enumerate(cases):
+        img = rng.uniform(lo, hi, (h, w))
+        if k % 2 == 0:
+            img = img.astype(np.float32).astype(np.float64)
+        mode = rs.Box(sp[1]) if sp[0] == "box" else rs.FirGaussian(sp[1], sp[2])
+        out[f"img_{k}"] = img
+        out[f"par_{k}"] = np.array([0 if sp[0] == "box" else 1, sp[1],
+                                    sp[1] if sp[0] == "box" else sp[2],
+                                    -1 if rad is None else rad, sr])
+        out[f"out_{k}"] = direct_bf(img, mode, gaussian_range(sr), radius=rad)
+    np.savez_compressed(os.path.join(HERE, "direct.npz"), **out)
+
+
 def big_plans():
     rows = []
     specs = [(2, 0, 5.0, 10.0), (3, 0, 8.0, 800.0)] + [(4, i, 6.0, 20.0) for i in range(64)] \
@@ -196,13 +225,17 @@ def big_plans():
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
+    ap.add_argument("--direct", action="store_true", help="only the direct_bf fixtures")
     a = ap.parse_args()
-    if not a.big:
+    if a.direct:
+        direct_cases()
+    elif not a.big:
         plans()
         maxfilters()
         smoothing()
         bf_cases()
         config1()
+        direct_cases()
     if a.big:
         big_plans()
     print("done")

@@ -106,4 +106,24 @@ def test_cli_compute_t_and_unsupported(tmp_path, capsys):
     assert cli.main(["compute-t", "--input", src, "--radius", "4"]) == 0
     assert f"T={O.compute_T(img, 4):g}" in capsys.readouterr().out
     assert cli.main(["filter", "--input", src, "--output", src + ".o", "--sigma-s", "2",
-                     "--sigma-r", "30", "--method", "direct"]) == 4
+                     "--sigma-r", "30", "--kernel", "poly"]) == 4
+
+
+@pytest.mark.gpu
+def test_cli_direct_method_and_bench_with_direct(tmp_path, capsys):
+    rng = np.random.default_rng(4)
+    img = np.round(rng.uniform(0, 255, (40, 44)))
+    src, raw = str(tmp_path / "in.pgm"), str(tmp_path / "d.f8")
+    save_pgm(img, src)
+    assert cli.main(["filter", "--input", src, "--output", src + ".o", "--sigma-s", "2",
+                     "--sigma-r", "30", "--method", "direct", "--float-out", raw]) == 0
+    got = np.fromfile(raw, dtype="<f8").reshape(img.shape)
+    R = O.support_radius("iterated", 2.0, 3)
+    ref = O.direct_bf(img, ("fir", 2.0, R), 30.0)
+    assert np.abs(got - ref).max() <= 1e-2
+    assert "method=direct" in capsys.readouterr().out
+    log = str(tmp_path / "b.csv")
+    assert cli.main(["bench", "--input", src, "--sigma-s", "2", "--sigma-r", "20,40",
+                     "--repeats", "1", "--with-direct", "--csv", log]) == 0
+    rows = list(csv.reader(open(log)))[1:]
+    assert len(rows) == 2 and all(float(r[9]) < 5.0 for r in rows)

@@ -238,3 +238,40 @@ def test_config_full_size_vs_c_oracle(cfg, size, idx):
     scale = max(1.0, float(np.abs(img).max()) / 255.0)
     mx, rms = assert_close_image(res.image, ref["image"], MAX_ABS * scale, RMS * scale)
     print(f"cfg{cfg} {img.shape}: max {mx:.3g} rms {rms:.3g} (scale {scale:.3g})")
+
+
+@pytest.mark.parametrize("k", range(8))
+def test_direct_bf_vs_reference_golden(k):
+    g = golden("direct.npz")
+    kind, a, b, rad, sr = g[f"par_{k}"]
+    mode = P.Box(int(b)) if kind == 0 else P.FirGaussian(float(a), int(b))
+    img = g[f"img_{k}"]
+    out = P.direct_bf(img, mode, P.gaussian_range(float(sr)), radius=None if rad < 0 else int(rad))
+    assert out.dtype == np.float64 and out.shape == img.shape
+    scale = max(1.0, float(np.abs(img).max()) / 255.0)
+    assert_close_image(out, g[f"out_{k}"], MAX_ABS * scale, RMS * scale)
+
+
+def test_direct_bf_full_size_vs_shiftable():
+    """The accuracy check direct_bf exists for: the shiftable filter vs the
+    brute-force Gaussian BF at config-2 size (reference acceptance-6 style)."""
+    import torch
+    img = torch.from_numpy(config_image(2)).cuda()
+    R = 15
+    ref = P.direct_bf(img, P.FirGaussian(5.0, R), P.gaussian_range(10.0))
+    ora = O.direct_bf(img[:96, :96].double().cpu().numpy(), ("fir", 5.0, R), 10.0)
+    d = ref[:96 - R, :96 - R].double().cpu().numpy() - ora[:96 - R, :96 - R]
+    assert float(np.abs(d).max()) < 1e-2
+    res = P.shiftable_bf(img, P.FilterParams(sigma_s=5, sigma_r=10, epsilon=0.01))
+    m = P.metrics(res.image, ref)
+    print(f"shiftable vs direct (FIR Gaussian, R={R}): mse {m.mse:.4g} max {m.max_abs:.4g}")
+    assert m.mse < 10.0
+
+
+def test_direct_bf_rejects_unsupported():
+    with pytest.raises(P.InvalidParameterError):
+        P.direct_bf(np.zeros((4, 4)), P.IteratedBox(2.0), P.gaussian_range(10.0), radius=3)
+    with pytest.raises(P.InvalidParameterError):
+        P.direct_bf(np.zeros((4, 4)), P.Box(1), lambda s: s)
+    with pytest.raises(P.InvalidParameterError):
+        P.direct_bf(np.full((4, 4), np.nan), P.Box(1), P.gaussian_range(10.0))

@@ -148,3 +148,17 @@ def test_band_split_is_exact():
     split = _oracle_par.shiftable_bf_full(img, 5.0, 10.0, 0.01, procs=4)
     assert (split["T"], split["N"], split["M"]) == (whole["T"], whole["N"], whole["M"])
     np.testing.assert_allclose(split["image"], whole["image"], rtol=0, atol=1e-9)
+
+
+def _direct_spatial(par):
+    kind, a, b, rad, sr = par
+    sp = ("box", int(b)) if kind == 0 else ("fir", float(a), int(b))
+    return sp, (None if rad < 0 else int(rad)), float(sr)
+
+
+@pytest.mark.parametrize("k", range(8))
+def test_direct_bf_matches_reference(k):
+    g = golden("direct.npz")
+    sp, rad, sr = _direct_spatial(g[f"par_{k}"])
+    out = O.direct_bf(g[f"img_{k}"], sp, sr, radius=rad)
+    np.testing.assert_allclose(out, g[f"out_{k}"], rtol=1e-12, atol=1e-9)
