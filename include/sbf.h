@@ -212,6 +212,27 @@ int sbf_direct_bf(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, in
                   const double* taps_host, double sigma_r, void* out, int out_dtype,
                   void* stream);
 
+/* ---- coarse non-local means (reference nlm.py:78-137) ----
+ * One item = one folded multi-index of the per-component expansions and one
+ * cos/sin choice for components j >= 1 (bit j of `mask`); component 0
+ * supplies the (cos, sin) pair.  weight = product of the folded component
+ * weights; turns[j] = w_j / (2 pi).  48 bytes. */
+typedef struct sbf_nlm_item {
+  double weight;
+  double turns[3];
+  int32_t mask;
+  int32_t pad;
+} sbf_nlm_item;
+
+/* Filters f with p (1..3) patch samples at `offsets` (host, 2p ints dy,dx;
+ * the first must be 0,0; replicate padding) over the host item table;
+ * stats = sbf_local_range statistics (centre) of f.  fp64 throughout;
+ * allocates its planes stream-ordered.  out/fallback: device. */
+int sbf_nlm_filter(const void* f, int dtype, int64_t H, int64_t W, int64_t ld,
+                   const sbf_spatial* sp, int p, const int32_t* offsets,
+                   const sbf_nlm_item* items, int n_items, const double* stats, void* out,
+                   int out_dtype, unsigned long long* fallback, void* stream);
+
 /* ---- introspection / benchmarking hooks ---- */
 int sbf_num_specialisations(void);
 int sbf_specialisation(int i, int* r, int* passes, int* mode);

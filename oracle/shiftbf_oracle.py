@@ -18,6 +18,7 @@ Each function cites the reference file:line it restates (paths relative to
 
 from __future__ import annotations
 
+import itertools
 import math
 from fractions import Fraction
 
@@ -346,6 +347,48 @@ def direct_bf(img, spatial, sigma_r, radius=None):
             den[yd, xd] += wr
     out, _ = divide_with_fallback(num, den, f)
     return out
+
+
+def _shifted_copy(f, offset):
+    """nlm.py:68-75 — f(x + u) with replicate padding."""
+    h, w = f.shape
+    rows = np.clip(np.arange(h) + offset[0], 0, h - 1)
+    cols = np.clip(np.arange(w) + offset[1], 0, w - 1)
+    return f[np.ix_(rows, cols)]
+
+
+def coarse_nlm(img, offsets, sigmas, spatial, radius, epsilon, truncation="auto"):
+    """nlm.py:78-137 (unfolded tensor product over all 2^p masks, as the
+    reference); budgets are checked by the caller.  `spatial` as in smooth().
+    Returns dict(image, T, plans=[(N, M)], fallback_pixels)."""
+    f = as_image(img)
+    R = int(radius) + max(max(abs(dy), abs(dx)) for dy, dx in offsets)
+    T = compute_T(f, R)
+    plans = [select_plan(T, s, epsilon, truncation) for s in sigmas]
+    comps = []
+    for (T_, N, M), sg, off in zip(plans, sigmas, offsets):
+        n, w, fr = raised_cosine_terms(N, M, sg)
+        fj = f if tuple(off) == (0, 0) else _shifted_copy(f, off)
+        comps.append([(wi, np.cos(om * fj), np.sin(om * fj)) for wi, om in zip(w, fr)])
+    p = len(offsets)
+    num = np.zeros_like(f)
+    den = np.zeros_like(f)
+    for combo in itertools.product(*comps):
+        weight = 1.0
+        for wi, _, _ in combo:
+            weight *= wi
+        cn = np.zeros_like(f)
+        cd = np.zeros_like(f)
+        for mask in range(1 << p):
+            aux = np.ones_like(f)
+            for j, (_, c, s_) in enumerate(combo):
+                aux = aux * (s_ if (mask >> j) & 1 else c)
+            cn += aux * smooth(f * aux, spatial)
+            cd += aux * smooth(aux, spatial)
+        num += weight * cn
+        den += weight * cd
+    out, n_bad = divide_with_fallback(num, den, f)
+    return dict(image=out, T=T, plans=[(N, M) for _, N, M in plans], fallback_pixels=n_bad)
 
 
 def metrics(a, b):

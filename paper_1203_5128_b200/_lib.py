@@ -81,6 +81,8 @@ _SIGS = {
     "sbf_pgm_decode": (_int, [_vp, _int, _i64, _vp, _vp]),
     "sbf_pgm_encode": (_int, [_vp, _int, _i64, _int, _vp, _vp]),
     "sbf_direct_bf": (_int, [_vp, _int, _i64, _i64, _i64, _int, _vp, _dbl, _vp, _int, _vp]),
+    "sbf_nlm_filter": (_int, [_vp, _int, _i64, _i64, _i64, C.POINTER(SbfSpatial), _int, _vp, _vp,
+                              _int, _vp, _vp, _int, _vp, _vp]),
     "sbf_fp32_probe": (_int, [_int, _int, _int, _vp, _vp]),
 }
 EXPORTS = tuple(_SIGS)

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "sbf_common.cuh"
+#include "sbf_generic.h"
 #include "sbf_generic_fused.cuh"
 
 namespace sbf {
@@ -166,6 +167,68 @@ __global__ void gen_accum(const double* __restrict__ planes, const void* f, int 
 
 }  // namespace
 
+// ---- reusable fp64 smoother of four planes (also used by coarse NLM) ----
+int PlaneSmoother::init(const sbf_spatial& sp, int64_t H_, int64_t W_, int64_t row0_,
+                        int64_t img_H_, cudaStream_t st) {
+  H = H_;
+  W = W_;
+  row0 = row0_;
+  img_H = img_H_;
+  passes = sp.mode == SBF_SPATIAL_BOX ? 1 : sp.passes;
+  alpha = sp.mode == SBF_SPATIAL_BOX ? 0.0 : sp.alpha;
+  r = sp.r;
+  static const FusedEntry fused_tab[] = {
+      {0, &launch_colpass<0>},   {1, &launch_colpass<1>},   {2, &launch_colpass<2>},
+      {3, &launch_colpass<3>},   {4, &launch_colpass<4>},   {5, &launch_colpass<5>},
+      {6, &launch_colpass<6>},   {7, &launch_colpass<7>},   {8, &launch_colpass<8>},
+      {9, &launch_colpass<9>},   {10, &launch_colpass<10>}, {11, &launch_colpass<11>},
+      {12, &launch_colpass<12>}};
+  fe = (passes == 3 && r >= 0 && r <= 12) ? &fused_tab[r] : nullptr;
+  fused = fe != nullptr;
+  gx = gy = nullptr;
+  if (fused) {
+    pad = 3 * (r + 1) + 2 * (r + 1) + 2;
+    const double cint = 2.0 * r + 1.0 + 2.0 * alpha;
+    ca = (1.0 - alpha) / cint;
+    cb = alpha / cint;
+    SBF_CHECK_CUDA(cudaMallocAsync(&gx, sizeof(double) * (W + 2 * pad), st));
+    SBF_CHECK_CUDA(cudaMallocAsync(&gy, sizeof(double) * (H + 2 * pad), st));
+    gfactor_table<<<(unsigned)((W + 2 * pad + 255) / 256), 256, 0, st>>>(gx, W, 0, W, r, alpha, pad);
+    gfactor_table<<<(unsigned)((H + 2 * pad + 255) / 256), 256, 0, st>>>(gy, H, row0, img_H, r,
+                                                                        alpha, pad);
+    SBF_CHECK_LAUNCH();
+  }
+  return SBF_OK;
+}
+
+int PlaneSmoother::run(double* planes, double* tmp, cudaStream_t st) const {
+  const int bs = 256;
+  const dim3 tb(32, 8);
+  if (fused) {
+    // input: tmp [pl][W][H] (rows as columns); output planes [pl][H][W]
+    const dim3 tgridT((unsigned)((H + 31) / 32), (unsigned)((W + 31) / 32), 4);
+    const int64_t seg = 256;
+    fe->launch(tmp, planes, 4, W, H, seg, gx, 0, W, ca, cb, st);                // row passes
+    transpose_planes<<<tgridT, tb, 0, st>>>(planes, tmp, W, H);                 // -> [pl][H][W]
+    fe->launch(tmp, planes, 4, H, W, seg, gy, row0, img_H, ca, cb, st);         // column passes
+  } else {
+    // input and output: planes [pl][H][W]
+    for (int ps = 0; ps < passes; ++ps) {
+      gen_rows<<<(unsigned)((4 * H + bs - 1) / bs), bs, 0, st>>>(planes, tmp, 4 * H, W, r, alpha);
+      gen_cols<<<(unsigned)((4 * W + bs - 1) / bs), bs, 0, st>>>(tmp, planes, 4, H, W, row0, img_H,
+                                                                 r, alpha);
+    }
+  }
+  SBF_CHECK_LAUNCH();
+  return SBF_OK;
+}
+
+void PlaneSmoother::release(cudaStream_t st) {
+  if (gx) cudaFreeAsync(gx, st);
+  if (gy) cudaFreeAsync(gy, st);
+  gx = gy = nullptr;
+}
+
 int launch_generic_terms(const FilterLaunch& a, double* nd) {
   cudaStream_t st = a.stream;
   sbf_plan plan;
@@ -185,57 +248,24 @@ int launch_generic_terms(const FilterLaunch& a, double* nd) {
   SBF_CHECK_CUDA(cudaMallocAsync(&tmp, sizeof(double) * 4 * n, st));
   const int bs = 256;
   const unsigned gpix = (unsigned)smin<int64_t>((n + bs - 1) / bs, 148 * 16);
-  const int passes = a.sp.mode == SBF_SPATIAL_BOX ? 1 : a.sp.passes;
-  const double alpha = a.sp.mode == SBF_SPATIAL_BOX ? 0.0 : a.sp.alpha;
-  const FusedEntry* fe = nullptr;
-  static const FusedEntry fused[] = {
-      {0, &launch_colpass<0>},   {1, &launch_colpass<1>},   {2, &launch_colpass<2>},
-      {3, &launch_colpass<3>},   {4, &launch_colpass<4>},   {5, &launch_colpass<5>},
-      {6, &launch_colpass<6>},   {7, &launch_colpass<7>},   {8, &launch_colpass<8>},
-      {9, &launch_colpass<9>},   {10, &launch_colpass<10>}, {11, &launch_colpass<11>},
-      {12, &launch_colpass<12>}};
-  if (passes == 3 && a.sp.r >= 0 && a.sp.r <= 12) fe = &fused[a.sp.r];
-  if (fe) {
-    // fused 3-pass cascade: rows on transposed planes, then columns
-    const int r = a.sp.r, pad = 3 * (r + 1) + 2 * (r + 1) + 2;
-    const double cint = 2.0 * r + 1.0 + 2.0 * alpha;
-    const double ca = (1.0 - alpha) / cint, cb = alpha / cint;
-    double *gx = nullptr, *gy = nullptr;
-    SBF_CHECK_CUDA(cudaMallocAsync(&gx, sizeof(double) * (W + 2 * pad), st));
-    SBF_CHECK_CUDA(cudaMallocAsync(&gy, sizeof(double) * (H + 2 * pad), st));
-    gfactor_table<<<(unsigned)((W + 2 * pad + 255) / 256), 256, 0, st>>>(gx, W, 0, W, r, alpha, pad);
-    gfactor_table<<<(unsigned)((H + 2 * pad + 255) / 256), 256, 0, st>>>(gy, H, a.row0, a.img_H, r,
-                                                                        alpha, pad);
-    const dim3 tb(32, 8), tgrid((unsigned)((W + 31) / 32), (unsigned)((H + 31) / 32), 1);
-    const dim3 tgridT((unsigned)((H + 31) / 32), (unsigned)((W + 31) / 32), 4);
-    const int64_t seg = 256;
-    for (int k = 0; k < plan.K_eval; ++k) {
+  PlaneSmoother sm;
+  int rc = sm.init(a.sp, H, W, a.row0, a.img_H, st);
+  if (rc != SBF_OK) return rc;
+  const dim3 tb(32, 8), tgrid((unsigned)((W + 31) / 32), (unsigned)((H + 31) / 32), 1);
+  for (int k = 0; k < plan.K_eval; ++k) {
+    if (sm.fused)
       gen_images_T<<<tgrid, tb, 0, st>>>(a.f, a.dtype == SBF_F64, H, W, a.ld, a.stats,
-                                         terms[k].turns, tmp);           // [pl][W][H]
-      fe->launch(tmp, planes, 4, W, H, seg, gx, 0, W, ca, cb, st);       // row passes
-      transpose_planes<<<tgridT, tb, 0, st>>>(planes, tmp, W, H);        // -> [pl][H][W]
-      fe->launch(tmp, planes, 4, H, W, seg, gy, a.row0, a.img_H, ca, cb, st);  // column passes
-      gen_accum<<<gpix, bs, 0, st>>>(planes, a.f, a.dtype == SBF_F64, H, W, a.ld, a.out_lo,
-                                     a.out_hi, a.stats, terms[k].turns, terms[k].scale, k == 0, nd);
-      SBF_CHECK_LAUNCH();
-    }
-    SBF_CHECK_CUDA(cudaFreeAsync(gx, st));
-    SBF_CHECK_CUDA(cudaFreeAsync(gy, st));
-  } else {
-    for (int k = 0; k < plan.K_eval; ++k) {
+                                         terms[k].turns, tmp);  // [pl][W][H]
+    else
       gen_images<<<gpix, bs, 0, st>>>(a.f, a.dtype == SBF_F64, H, W, a.ld, a.stats,
                                       terms[k].turns, planes);
-      for (int ps = 0; ps < passes; ++ps) {
-        gen_rows<<<(unsigned)((4 * H + bs - 1) / bs), bs, 0, st>>>(planes, tmp, 4 * H, W, a.sp.r,
-                                                                   alpha);
-        gen_cols<<<(unsigned)((4 * W + bs - 1) / bs), bs, 0, st>>>(tmp, planes, 4, H, W, a.row0,
-                                                                   a.img_H, a.sp.r, alpha);
-      }
-      gen_accum<<<gpix, bs, 0, st>>>(planes, a.f, a.dtype == SBF_F64, H, W, a.ld, a.out_lo,
-                                     a.out_hi, a.stats, terms[k].turns, terms[k].scale, k == 0, nd);
-      SBF_CHECK_LAUNCH();
-    }
+    rc = sm.run(planes, tmp, st);
+    if (rc != SBF_OK) return rc;
+    gen_accum<<<gpix, bs, 0, st>>>(planes, a.f, a.dtype == SBF_F64, H, W, a.ld, a.out_lo,
+                                   a.out_hi, a.stats, terms[k].turns, terms[k].scale, k == 0, nd);
+    SBF_CHECK_LAUNCH();
   }
+  sm.release(st);
   SBF_CHECK_CUDA(cudaFreeAsync(planes, st));
   SBF_CHECK_CUDA(cudaFreeAsync(tmp, st));
   return SBF_OK;

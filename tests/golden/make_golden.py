@@ -207,6 +207,31 @@ def direct_cases():
     np.savez_compressed(os.path.join(HERE, "direct.npz"), **out)
 
 
+def nlm_cases():
+    """coarse_nlm_shiftable (nlm.py:78-137) on small images."""
+    from shiftbf import nlm as rn
+    rng = np.random.default_rng(20260812)
+    cases = [
+        # (h, w, offsets, sigmas, spatial, radius, eps)
+        (24, 28, [(0, 0)], [20.0], ("iter", 2.0), 6, 0.05),
+        (20, 22, [(0, 0), (0, 1)], [40.0, 40.0], ("iter", 2.0), 6, 0.05),
+        (18, 18, [(0, 0), (1, -1)], [50.0, 35.0], ("box", 2), 2, 0.05),
+        (16, 19, [(0, 0), (0, 1), (1, 0)], [60.0, 60.0, 60.0], ("iter", 1.5), 5, 0.1),
+        (22, 20, [(0, 0), (2, 0)], [80.0, 45.0], ("iter", 3.0), 9, 0.0),
+    ]
+    out = {}
+    for k, (h, w, offs, sgs, sp, rad, eps) in enumerate(cases):
+        img = rng.uniform(0, 120, (h, w))
+        mode = rs.Box(sp[1]) if sp[0] == "box" else rs.IteratedBox(sp[1])
+        res = rn.coarse_nlm_shiftable(img, rn.PatchSpec(tuple(offs), tuple(sgs)), mode, rad, eps)
+        out[f"img_{k}"] = img
+        out[f"offs_{k}"] = np.array(offs, dtype=np.int64)
+        out[f"par_{k}"] = np.array(sgs + [0 if sp[0] == "box" else 1, sp[1], rad, eps])
+        out[f"out_{k}"] = res.image
+        out[f"plans_{k}"] = np.array([[p.T, p.N, p.M] for p in res.plans])
+    np.savez_compressed(os.path.join(HERE, "nlm.npz"), **out)
+
+
 def big_plans():
     rows = []
     specs = [(2, 0, 5.0, 10.0), (3, 0, 8.0, 800.0)] + [(4, i, 6.0, 20.0) for i in range(64)] \
@@ -229,6 +254,7 @@ if __name__ == "__main__":
     a = ap.parse_args()
     if a.direct:
         direct_cases()
+        nlm_cases()
     elif not a.big:
         plans()
         maxfilters()
@@ -236,6 +262,7 @@ if __name__ == "__main__":
         bf_cases()
         config1()
         direct_cases()
+        nlm_cases()
     if a.big:
         big_plans()
     print("done")

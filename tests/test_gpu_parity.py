@@ -275,3 +275,37 @@ def test_direct_bf_rejects_unsupported():
         P.direct_bf(np.zeros((4, 4)), P.Box(1), lambda s: s)
     with pytest.raises(P.InvalidParameterError):
         P.direct_bf(np.full((4, 4), np.nan), P.Box(1), P.gaussian_range(10.0))
+
+
+@pytest.mark.parametrize("k", range(5))
+def test_coarse_nlm_vs_reference_golden(k):
+    g = golden("nlm.npz")
+    offs = [tuple(int(v) for v in o) for o in g[f"offs_{k}"]]
+    par = g[f"par_{k}"]
+    p = len(offs)
+    kind, a, rad, eps = par[p:]
+    mode = P.Box(int(a)) if kind == 0 else P.IteratedBox(float(a))
+    res = P.coarse_nlm_shiftable(g[f"img_{k}"], P.PatchSpec(tuple(offs), tuple(par[:p])), mode,
+                                 int(rad), float(eps))
+    assert [(pl.T, pl.N, pl.M) for pl in res.plans] == [tuple(r) for r in g[f"plans_{k}"].tolist()]
+    assert_close_image(res.image, g[f"out_{k}"])
+
+
+def test_coarse_nlm_single_offset_is_the_bilateral_filter():
+    img = config_image(2, size=96)
+    a = P.coarse_nlm_shiftable(img, P.PatchSpec(((0, 0),), (60.0,)), P.IteratedBox(3.0), 9, 0.05,
+                               max_component_order=64)
+    b = P.shiftable_bf(img, P.FilterParams(sigma_s=3, sigma_r=60, epsilon=0.05, window_radius=9))
+    assert (a.plans[0].N, a.plans[0].M) == (b.plan.N, b.plan.M)
+    assert_close_image(a.image, b.image)
+
+
+def test_coarse_nlm_budgets():
+    img = np.random.default_rng(0).uniform(0, 255, (16, 16))
+    with pytest.raises(P.TermBudgetError):
+        P.coarse_nlm_shiftable(img, P.PatchSpec(((0, 0),), (5.0,)), P.IteratedBox(2.0), 4, 0.01)
+    with pytest.raises(P.TermBudgetError):
+        P.coarse_nlm_shiftable(img, P.PatchSpec(((0, 0), (0, 1), (1, 0)), (90.0, 90.0, 90.0)),
+                               P.IteratedBox(2.0), 4, 0.0, term_budget=10)
+    with pytest.raises(P.InvalidParameterError):
+        P.PatchSpec(((1, 0),), (10.0,))

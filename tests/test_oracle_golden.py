@@ -162,3 +162,37 @@ def test_direct_bf_matches_reference(k):
     sp, rad, sr = _direct_spatial(g[f"par_{k}"])
     out = O.direct_bf(g[f"img_{k}"], sp, sr, radius=rad)
     np.testing.assert_allclose(out, g[f"out_{k}"], rtol=1e-12, atol=1e-9)
+
+
+def _nlm_case(g, k):
+    offs = [tuple(int(v) for v in o) for o in g[f"offs_{k}"]]
+    par = g[f"par_{k}"]
+    p = len(offs)
+    sg = [float(v) for v in par[:p]]
+    kind, a, rad, eps = par[p:]
+    sp = ("box", int(a)) if kind == 0 else ("iterated", float(a), 3)
+    return offs, sg, sp, int(rad), float(eps)
+
+
+@pytest.mark.parametrize("k", range(5))
+def test_coarse_nlm_matches_reference(k):
+    g = golden("nlm.npz")
+    offs, sg, sp, rad, eps = _nlm_case(g, k)
+    res = O.coarse_nlm(g[f"img_{k}"], offs, sg, sp, rad, eps)
+    assert [(res["T"], N, M) for N, M in res["plans"]] == [tuple(r) for r in g[f"plans_{k}"].tolist()]
+    np.testing.assert_allclose(res["image"], g[f"out_{k}"], rtol=1e-10, atol=1e-8)
+
+
+def test_nlm_item_table_folding():
+    """Folding +-w per component keeps the tensor product exact."""
+    from paper_1203_5128_b200 import kernels as K
+    from paper_1203_5128_b200.nlm import _folded
+    for N, M in ((7, 0), (15, 3), (4, 1)):
+        plan = K.KernelPlan(K.KernelFamily.RAISED_COSINE, 10.0, 100.0, N, M, 0.01 if M else 0.0)
+        fold = _folded(plan)
+        e = K.raised_cosine_expansion(plan)
+        # sum_n d_n cos(w_n s) == sum_folded scale cos(2 pi turns s) for sample s
+        for s in (0.0, 1.3, 17.0, -40.5):
+            full = float(np.sum(e.weights * np.cos(e.frequencies * s)))
+            folded = sum(sc * math.cos(2 * math.pi * t * s) for sc, t in fold)
+            assert abs(full - folded) < 1e-12
