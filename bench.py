@@ -305,7 +305,8 @@ def run_ours(args, rank, world, dev):
         e2e_total = float(t.item())
     e2e_value = world * px * args.steps / (e2e_total * 1e-3) / 1e6
     h2d = img_np.nbytes
-    d2h = px * 8 + 64 + 64 + 8  # float64 result + plan + stats + fallback counter
+    # result (the input's float dtype for torch input) + plan + stats + fallback counter
+    d2h = px * res.image.element_size() + 64 + 64 + 8
 
     peak_meas, sms = fp32_peak(lib, torch, dev)
     peak_meas2, _ = fp32_peak(lib, torch, dev, packed=True)

@@ -98,12 +98,15 @@ def shiftable_bf(img, params: FilterParams) -> ShiftableResult:
     fallback (RuntimeWarning + count).
     """
     s = stage(img)
-    out, plan, fallbacks = _filter_staged(s, params, out_f64=(s.host or s.dtype == _lib.SBF_F64),
+    numpy_in = s.host and not s.torch_in
+    out, plan, fallbacks = _filter_staged(s, params, out_f64=(numpy_in or s.dtype == _lib.SBF_F64),
                                           to_host=s.host)
     if fallbacks:
         warnings.warn(f"{fallbacks} pixel(s) had a non-positive normalizer; input values kept",
                       RuntimeWarning, stacklevel=2)
-    result = out.numpy() if s.host else out
+    # numpy in -> float64 numpy out (reference semantics); torch in -> torch
+    # out in the input's float dtype, on the input's side (pinned host / CUDA)
+    result = out.numpy() if numpy_in else out
     return ShiftableResult(result, plan, fallbacks)
 
 

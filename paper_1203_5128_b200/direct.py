@@ -73,8 +73,8 @@ def _taps(mode, radius):
 def direct_bf(img, spatial, range_kernel, radius=None):
     """Brute-force bilateral filter over the clamped window (bilateral.py:205-239).
 
-    Returns float64 numpy for host input, a CUDA tensor (input float dtype)
-    for CUDA tensor input.
+    Returns float64 numpy for numpy input; torch input gives a torch tensor
+    in the input float dtype on the input's device.
     """
     import torch
 
@@ -92,7 +92,8 @@ def direct_bf(img, spatial, range_kernel, radius=None):
     taps = _taps(spatial, radius)
     s = stage(img)
     stats, _ = local_range(s, 0)  # input statistics: non-finite samples are rejected
-    out_f64 = s.host or s.dtype == _lib.SBF_F64
+    numpy_in = s.host and not s.torch_in
+    out_f64 = numpy_in or s.dtype == _lib.SBF_F64
     out = torch.empty((s.H, s.W), dtype=torch.float64 if out_f64 else torch.float32,
                       device=s.tensor.device)
     lib = _lib.load()
@@ -103,7 +104,7 @@ def direct_bf(img, spatial, range_kernel, radius=None):
                "direct_bf")
     if int(stats[7:8].cpu().view(torch.int64).item()) != 0:
         raise InvalidParameterError("image contains non-finite samples")
-    return out.cpu().numpy() if s.host else out
+    return out.cpu().numpy() if numpy_in else (out.cpu() if s.host else out)
 
 
 @dataclass(frozen=True)

@@ -54,6 +54,7 @@ class Staged:
     host: bool           # caller passed a host array
     H: int
     W: int
+    torch_in: bool = False  # caller passed a torch tensor (results keep its float dtype)
 
 
 def stage(img, device=None) -> Staged:
@@ -71,7 +72,8 @@ def stage(img, device=None) -> Staged:
             exact32 = t.dtype in (torch.uint8, torch.int8, torch.int16, torch.bool)
             t = t.to(torch.float32 if exact32 else torch.float64)
         if host:
-            t = t.to(device or "cuda", non_blocking=False)
+            # pinned sources copy asynchronously, ordered before K1 on the stream
+            t = t.contiguous().to(device or "cuda", non_blocking=t.is_pinned())
         t = t.contiguous()
     else:
         a = np.asarray(img)
@@ -86,4 +88,4 @@ def stage(img, device=None) -> Staged:
         t = torch.from_numpy(a).to(device or "cuda")
         host = True
     dt = _lib.SBF_F64 if t.dtype == torch.float64 else _lib.SBF_F32
-    return Staged(t, dt, host, int(t.shape[0]), int(t.shape[1]))
+    return Staged(t, dt, host, int(t.shape[0]), int(t.shape[1]), isinstance(img, torch.Tensor))

@@ -116,7 +116,8 @@ def coarse_nlm_shiftable(img, patch: PatchSpec, spatial: SpatialMode, radius: in
                          term_budget: int = DEFAULT_TERM_BUDGET) -> NlmResult:
     """Constant-time coarse non-local means (nlm.py:78-137) on the GPU.
 
-    Returns float64 numpy for host input, a CUDA tensor for CUDA input.
+    Returns float64 numpy for numpy input; torch input gives a torch tensor
+    in the input float dtype on the input's device.
     With a single origin offset this is the bilateral filter.
     """
     import torch
@@ -145,7 +146,8 @@ def coarse_nlm_shiftable(img, patch: PatchSpec, spatial: SpatialMode, radius: in
             f"exceeding the term budget of {term_budget}")
     items, n_items = build_items(plans)
     offs = (C.c_int32 * (2 * patch.size))(*[v for off in patch.offsets for v in off])
-    out_f64 = s.host or s.dtype == _lib.SBF_F64
+    numpy_in = s.host and not s.torch_in
+    out_f64 = numpy_in or s.dtype == _lib.SBF_F64
     out = torch.empty((s.H, s.W), dtype=torch.float64 if out_f64 else torch.float32,
                       device=s.tensor.device)
     fb = torch.zeros(1, dtype=torch.int64, device=s.tensor.device)
@@ -159,4 +161,4 @@ def coarse_nlm_shiftable(img, patch: PatchSpec, spatial: SpatialMode, radius: in
     if fallbacks:
         warnings.warn(f"{fallbacks} pixel(s) had a non-positive normalizer; input values kept",
                       RuntimeWarning, stacklevel=2)
-    return NlmResult(out.cpu().numpy() if s.host else out, plans, fallbacks)
+    return NlmResult(out.cpu().numpy() if numpy_in else (out.cpu() if s.host else out), plans, fallbacks)
