@@ -207,10 +207,12 @@ int sbf_pgm_encode(const void* img_dev, int dtype, int64_t n, int maxval, void* 
  * gaussian_range(sigma_r), radius)`: out(x) = sum_y w(y) g(f(y)-f(x)) f(y) /
  * sum_y w(y) g(...) over the in-bounds (2R+1)^2 window, g Gaussian of width
  * sigma_r, w(dy,dx) = taps[dy+R] taps[dx+R] (taps == NULL: uniform, the Box
- * mode; spatial.py:197-213).  R <= 255.  Device buffers, stream-ordered. */
+ * mode; spatial.py:197-213).  R <= 255.  precision SBF_PREC_FP32 (fp32
+ * math, log2-domain weights) or SBF_PREC_HDR (fp64, the reference's
+ * arithmetic).  Device buffers, stream-ordered. */
 int sbf_direct_bf(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int R,
-                  const double* taps_host, double sigma_r, void* out, int out_dtype,
-                  void* stream);
+                  const double* taps_host, double sigma_r, int precision, void* out,
+                  int out_dtype, void* stream);
 
 /* ---- coarse non-local means (reference nlm.py:78-137) ----
  * One item = one folded multi-index of the per-component expansions and one

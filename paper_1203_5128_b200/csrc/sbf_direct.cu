@@ -12,6 +12,7 @@
 // (a zero tap gives -inf, i.e. weight 0, as in the reference).  Only in-bounds
 // neighbours contribute (the reference's offset_slices), num / den in fp32,
 // den <= 0 (impossible with the positive Gaussian) falls back to the input.
+// Wide-range (HDR) images run an fp64 twin with the reference's arithmetic.
 #include "sbf_common.cuh"
 
 namespace sbf {
@@ -24,7 +25,40 @@ struct DirectParams {
   int R;
   float c;                      // -log2(e) / (2 sigma_r^2)
   float ltap[2 * kDirectMaxR + 1];  // log2 of the 1-D taps
+  double inv;                   // 1 / (2 sigma_r^2)   (fp64 variant)
+  double tap[2 * kDirectMaxR + 1];  // the 1-D taps       (fp64 variant)
 };
+
+// fp64 twin for wide intensity ranges (HDR): the reference's own arithmetic,
+// w = tap[dy] tap[dx] exp(-d^2 / (2 sr^2)), accumulated in float64.
+template <typename FT, typename OT>
+__global__ void __launch_bounds__(256) direct_kernel_f64(const FT* __restrict__ f,
+                                                         OT* __restrict__ out,
+                                                         const __grid_constant__ DirectParams p) {
+  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t y = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= p.W || y >= p.H) return;
+  const int R = p.R;
+  const double c = (double)f[y * p.ld + x];
+  const int dx_lo = (int)smax<int64_t>(-R, -x), dx_hi = (int)smin<int64_t>(R, p.W - 1 - x);
+  const int dy_lo = (int)smax<int64_t>(-R, -y), dy_hi = (int)smin<int64_t>(R, p.H - 1 - y);
+  double num = 0.0, den = 0.0;
+  for (int dy = dy_lo; dy <= dy_hi; ++dy) {
+    const FT* row = f + (y + dy) * p.ld + x;
+    const double wy = p.tap[dy + R];
+    if (wy == 0.0) continue;
+    for (int dx = dx_lo; dx <= dx_hi; ++dx) {
+      const double wsp = wy * p.tap[dx + R];
+      if (wsp == 0.0) continue;
+      const double v = (double)row[dx];
+      const double d = v - c;
+      const double w = wsp * exp(-(d * d) * p.inv);
+      num += w * v;
+      den += w;
+    }
+  }
+  out[y * p.W + x] = (OT)(den > 0.0 ? num / den : c);
+}
 
 template <typename FT, typename OT>
 __global__ void __launch_bounds__(256) direct_kernel(const FT* __restrict__ f, OT* __restrict__ out,
@@ -65,10 +99,17 @@ __global__ void __launch_bounds__(256) direct_kernel(const FT* __restrict__ f, O
 }
 
 template <typename FT, typename OT>
-int launch_direct(const void* f, void* out, const DirectParams& p, cudaStream_t st) {
+int launch_direct(const void* f, void* out, const DirectParams& p, int f64math, cudaStream_t st) {
   dim3 block(32, 8);
-  dim3 grid((unsigned)((p.W + 31) / 32), (unsigned)((p.H + 15) / 16));
-  direct_kernel<FT, OT><<<grid, block, 0, st>>>(static_cast<const FT*>(f), static_cast<OT*>(out), p);
+  if (f64math) {
+    dim3 grid((unsigned)((p.W + 31) / 32), (unsigned)((p.H + 7) / 8));
+    direct_kernel_f64<FT, OT><<<grid, block, 0, st>>>(static_cast<const FT*>(f),
+                                                      static_cast<OT*>(out), p);
+  } else {
+    dim3 grid((unsigned)((p.W + 31) / 32), (unsigned)((p.H + 15) / 16));
+    direct_kernel<FT, OT><<<grid, block, 0, st>>>(static_cast<const FT*>(f), static_cast<OT*>(out),
+                                                  p);
+  }
   SBF_CHECK_LAUNCH();
   return SBF_OK;
 }
@@ -77,8 +118,8 @@ int launch_direct(const void* f, void* out, const DirectParams& p, cudaStream_t 
 }  // namespace sbf
 
 extern "C" int sbf_direct_bf(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int R,
-                             const double* taps, double sigma_r, void* out, int out_dtype,
-                             void* stream) {
+                             const double* taps, double sigma_r, int precision, void* out,
+                             int out_dtype, void* stream) {
   using namespace sbf;
   SBF_REQUIRE(f && out, SBF_ERR_INVALID, "null pointer");
   SBF_REQUIRE(dtype == SBF_F32 || dtype == SBF_F64, SBF_ERR_INVALID, "bad dtype");
@@ -93,16 +134,21 @@ extern "C" int sbf_direct_bf(const void* f, int dtype, int64_t H, int64_t W, int
   p.W = W;
   p.ld = ld;
   p.R = R;
+  SBF_REQUIRE(precision == SBF_PREC_FP32 || precision == SBF_PREC_HDR, SBF_ERR_INVALID,
+              "bad precision mode");
   p.c = (float)(-1.4426950408889634 / (2.0 * sigma_r * sigma_r));
+  p.inv = 1.0 / (2.0 * sigma_r * sigma_r);
   for (int k = 0; k <= 2 * R; ++k) {
     const double t = taps ? taps[k] : 1.0;
     SBF_REQUIRE(t >= 0.0 && t == t, SBF_ERR_INVALID, "spatial taps must be non-negative");
     p.ltap[k] = t > 0.0 ? (float)log2(t) : -INFINITY;
+    p.tap[k] = t;
   }
+  const int f64math = precision == SBF_PREC_HDR;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (dtype == SBF_F32)
-    return out_dtype == SBF_F32 ? launch_direct<float, float>(f, out, p, st)
-                                : launch_direct<float, double>(f, out, p, st);
-  return out_dtype == SBF_F32 ? launch_direct<double, float>(f, out, p, st)
-                              : launch_direct<double, double>(f, out, p, st);
+    return out_dtype == SBF_F32 ? launch_direct<float, float>(f, out, p, f64math, st)
+                                : launch_direct<float, double>(f, out, p, f64math, st);
+  return out_dtype == SBF_F32 ? launch_direct<double, float>(f, out, p, f64math, st)
+                              : launch_direct<double, double>(f, out, p, f64math, st);
 }

@@ -19,7 +19,8 @@ import numpy as np
 from . import _lib
 from .errors import InvalidParameterError
 from .image import as_image, stage
-from .maxfilter import _stream_ptr, local_range
+from .bilateral import HDR_THRESHOLD
+from .maxfilter import _nonfinite, _stream_ptr, local_range
 from .spatial import Box, FirGaussian, IteratedBox
 
 
@@ -92,6 +93,11 @@ def direct_bf(img, spatial, range_kernel, radius=None):
     taps = _taps(spatial, radius)
     s = stage(img)
     stats, _ = local_range(s, 0)  # input statistics: non-finite samples are rejected
+    st = stats.cpu().numpy()
+    if _nonfinite(st):
+        raise InvalidParameterError("image contains non-finite samples")
+    # fp32 math unless the intensities span more than the HDR threshold
+    hdr = max(abs(st[2] - st[3]), abs(st[1] - st[3])) > HDR_THRESHOLD
     numpy_in = s.host and not s.torch_in
     out_f64 = numpy_in or s.dtype == _lib.SBF_F64
     out = torch.empty((s.H, s.W), dtype=torch.float64 if out_f64 else torch.float32,
@@ -99,11 +105,10 @@ def direct_bf(img, spatial, range_kernel, radius=None):
     lib = _lib.load()
     _lib.check(lib.sbf_direct_bf(s.tensor.data_ptr(), s.dtype, s.H, s.W, s.W, radius,
                                  None if taps is None else taps.ctypes.data,
-                                 float(range_kernel.sigma_r), out.data_ptr(),
+                                 float(range_kernel.sigma_r),
+                                 _lib.PREC_HDR if hdr else _lib.PREC_FP32, out.data_ptr(),
                                  _lib.SBF_F64 if out_f64 else _lib.SBF_F32, _stream_ptr()),
                "direct_bf")
-    if int(stats[7:8].cpu().view(torch.int64).item()) != 0:
-        raise InvalidParameterError("image contains non-finite samples")
     return out.cpu().numpy() if numpy_in else (out.cpu() if s.host else out)
 
 

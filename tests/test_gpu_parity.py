@@ -235,9 +235,8 @@ def test_config_full_size_vs_c_oracle(cfg, size, idx):
     res = P.shiftable_bf(img, P.FilterParams(sigma_s=c[0], sigma_r=c[1], epsilon=0.01))
     ref = _oracle_par.shiftable_bf_full(img, c[0], c[1], 0.01)
     assert (res.plan.T, res.plan.N, res.plan.M) == (ref["T"], ref["N"], ref["M"])
-    scale = max(1.0, float(np.abs(img).max()) / 255.0)
-    mx, rms = assert_close_image(res.image, ref["image"], MAX_ABS * scale, RMS * scale)
-    print(f"cfg{cfg} {img.shape}: max {mx:.3g} rms {rms:.3g} (scale {scale:.3g})")
+    mx, rms = assert_close_image(res.image, ref["image"])  # absolute, in the image's own units
+    print(f"cfg{cfg} {img.shape}: max {mx:.3g} rms {rms:.3g}")
 
 
 @pytest.mark.parametrize("k", range(8))
@@ -248,8 +247,7 @@ def test_direct_bf_vs_reference_golden(k):
     img = g[f"img_{k}"]
     out = P.direct_bf(img, mode, P.gaussian_range(float(sr)), radius=None if rad < 0 else int(rad))
     assert out.dtype == np.float64 and out.shape == img.shape
-    scale = max(1.0, float(np.abs(img).max()) / 255.0)
-    assert_close_image(out, g[f"out_{k}"], MAX_ABS * scale, RMS * scale)
+    assert_close_image(out, g[f"out_{k}"])  # absolute gray levels, HDR included
 
 
 def test_direct_bf_full_size_vs_shiftable():
