@@ -236,6 +236,10 @@ int sbf_nlm_filter(const void* f, int dtype, int64_t H, int64_t W, int64_t ld,
                    int out_dtype, unsigned long long* fallback, void* stream);
 
 /* ---- introspection / benchmarking hooks ---- */
+/* fp64 (HDR / generic) evaluation, this thread: 0 = always the K term sweeps,
+ * 1 = cost model (default: the dual form cos(gamma s)^N over the (2S+1)^2
+ * window when M = 0 and it is cheaper), 2 = dual whenever M = 0. */
+int sbf_set_fp64_method(int mode);
 int sbf_num_specialisations(void);
 int sbf_specialisation(int i, int* r, int* passes, int* mode);
 int sbf_filter_geometry(int64_t rows_out, int64_t W, const sbf_spatial* sp, int precision,

@@ -6,6 +6,7 @@
 
 #include "sbf_common.cuh"
 #include "sbf_plan_logic.cuh"
+#include "sbf_generic.h"
 #include "sbf_terms.cuh"
 
 namespace sbf {
@@ -156,6 +157,9 @@ static int launch_epilogue(const FilterLaunch& a, const ACC* nd, int groups, int
 
 // stage mask for benchmarking: 1 = K3 term kernel, 2 = K4 epilogue (3 = both)
 static thread_local int g_stage_mask = 3;
+// fp64 evaluation choice: 0 = always the term sweeps, 1 = cost model, 2 = dual
+// whenever exact (M = 0)
+static thread_local int g_dual_mode = 1;
 
 int launch_filter(const FilterLaunch& a) {
   int r, passes;
@@ -183,6 +187,16 @@ int launch_filter(const FilterLaunch& a) {
   if (!e) {
     const size_t need = align_up((size_t)(rows_out * a.W) * 16);
     SBF_REQUIRE(a.ws && a.ws_bytes >= need, SBF_ERR_WORKSPACE, "filter workspace too small");
+    if (g_dual_mode != 0) {
+      // fp64 path: the plan decides between K term sweeps and the dual form
+      sbf_plan plan;
+      SBF_CHECK_CUDA(cudaMemcpyAsync(&plan, a.plan, sizeof(plan), cudaMemcpyDeviceToHost,
+                                     a.stream));
+      SBF_CHECK_CUDA(cudaStreamSynchronize(a.stream));
+      if (g_dual_mode == 2 ? (plan.status == SBF_OK && plan.M == 0 && plan.K_eval > 0)
+                           : dual_preferred(a, plan))
+        return launch_dual_direct(a, plan);
+    }
     double* nd = static_cast<double*>(a.ws);
     int rc = launch_generic_terms(a, nd);
     if (rc != SBF_OK) return rc;
@@ -257,6 +271,12 @@ int sbf_abi_version(void) { return SBF_ABI_VERSION; }
 int sbf_set_stage_mask(int mask) {
   if (mask < 1 || mask > 3) return SBF_ERR_INVALID;
   sbf::g_stage_mask = mask;
+  return SBF_OK;
+}
+
+int sbf_set_fp64_method(int mode) {
+  if (mode < 0 || mode > 2) return SBF_ERR_INVALID;
+  sbf::g_dual_mode = mode;
   return SBF_OK;
 }
 

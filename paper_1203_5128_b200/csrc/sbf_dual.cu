@@ -1,0 +1,313 @@
+// Dual (direct) evaluation of the shiftable filter for untruncated plans.
+//
+// With M = 0 the retained raised-cosine expansion sums to the closed form
+//     sum_n C(N,n)/2^N cos((2n-N) gamma s) = cos(gamma s)^N
+// (binomial theorem; reference kernels.py:198-227 — terms whose fp64 weight
+// underflows contribute < 1e-300).  By linearity of the smoother, the
+// reference's num/den (bilateral.py:140-164) are then exactly
+//     num(x) = sum_y A_r(x_r, y_r) A_c(x_c, y_c) cos(gamma (f(y)-f(x)))^N f(y)
+// (den likewise without f(y)), where A_r / A_c are the 1-D effective weights
+// of the spatial mode — `passes` extended-box passes with clamped
+// renormalisation (spatial.py:108-139) or the box filter (spatial.py:65-78);
+// rows and columns commute, so the 2-D weight is their product.
+//
+// That costs (2S+1)^2 taps per pixel instead of K terms of four smoothings,
+// so for high-order plans (HDR, config 3: N = 2463, K = 1232, S = 24) it is
+// the cheaper exact evaluation; the dispatcher picks it by a cost estimate.
+// Everything in fp64: for integer-valued images (16-bit HDR) cos(gamma s)^N
+// is tabulated per integer difference; otherwise cos(gamma s) comes from
+// per-pixel phasors (cos gamma f, sin gamma f) by the angle-difference
+// identity and the power by square-and-multiply (relative error ~N ulp).
+#include <math.h>
+
+#include <vector>
+
+#include "sbf_common.cuh"
+
+namespace sbf {
+namespace {
+
+// per-pixel (cos gamma f, sin gamma f)
+template <typename FT>
+__global__ void phasor_kernel(const FT* __restrict__ f, int64_t H, int64_t W, int64_t ld,
+                              const sbf_plan* __restrict__ plan, double2* __restrict__ P) {
+  const double g = plan->gamma;
+  const int64_t n = H * W;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t y = i / W, x = i - y * W;
+    double s, c;
+    sincos(g * (double)f[y * ld + x], &s, &c);
+    P[i] = make_double2(c, s);
+  }
+}
+
+__device__ __forceinline__ double pow_n(double c, int n) {
+  double r = 1.0;
+  while (n) {
+    if (n & 1) r *= c;
+    c *= c;
+    n >>= 1;
+  }
+  return r;
+}
+
+template <typename FT, typename OT>
+__global__ void __launch_bounds__(256) dual_kernel(const FT* __restrict__ f, int64_t H, int64_t W,
+                                                   int64_t ld, int64_t out_lo, int64_t out_hi,
+                                                   int S, const double* __restrict__ Wr,
+                                                   const double* __restrict__ Wc,
+                                                   const double2* __restrict__ P,
+                                                   const sbf_plan* __restrict__ plan,
+                                                   OT* __restrict__ out,
+                                                   unsigned long long* __restrict__ fallback) {
+  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t yo = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
+  const int64_t y = out_lo + yo;
+  bool bad = false;
+  if (x < W && y < out_hi) {
+    const int N = plan->N;
+    const int T = 2 * S + 1;
+    const double2 px = P[y * W + x];
+    const double* wr = Wr + yo * T;
+    const double* wc = Wc + x * T;
+    const int dy_lo = (int)smax<int64_t>(-S, -y), dy_hi = (int)smin<int64_t>(S, H - 1 - y);
+    const int dx_lo = (int)smax<int64_t>(-S, -x), dx_hi = (int)smin<int64_t>(S, W - 1 - x);
+    double num = 0.0, den = 0.0;
+    for (int dy = dy_lo; dy <= dy_hi; ++dy) {
+      const double a = wr[dy + S];
+      if (a == 0.0) continue;
+      const double2* prow = P + (y + dy) * W + x;
+      const FT* frow = f + (y + dy) * ld + x;
+      for (int dx = dx_lo; dx <= dx_hi; ++dx) {
+        const double2 q = prow[dx];
+        double c = fma(q.x, px.x, q.y * px.y);  // cos(gamma (f(y) - f(x)))
+        c = c > 1.0 ? 1.0 : (c < -1.0 ? -1.0 : c);
+        const double k = pow_n(c, N);  // odd N keeps the sign, as the expansion does
+        const double w = a * wc[dx + S] * k;
+        num = fma(w, (double)frow[dx], num);
+        den += w;
+      }
+    }
+    bad = !(den > 0.0);  // bilateral.py:244
+    out[yo * W + x] = (OT)(bad ? (double)f[y * ld + x] : num / den);
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(fallback, (unsigned long long)__popc(m));
+}
+
+// Integer-valued images (e.g. 16-bit HDR): the kernel depends on the integer
+// difference only, so cos(gamma s)^N is tabulated once for s in [0, smax]
+// (even in s) and every tap is one table read.
+template <typename FT>
+__global__ void integral_check(const FT* __restrict__ f, int64_t H, int64_t W, int64_t ld,
+                               int* __restrict__ non_integer) {
+  const int64_t n = H * W;
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t y = i / W, x = i - y * W;
+    const double v = (double)f[y * ld + x];
+    bad |= !(v == rint(v) && fabs(v) <= 16777216.0);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(non_integer, 1);
+}
+
+__global__ void kernel_table(const sbf_plan* __restrict__ plan, int64_t smax,
+                             double* __restrict__ lut) {
+  const double g = plan->gamma;
+  const int N = plan->N;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s <= smax;
+       s += (int64_t)gridDim.x * blockDim.x)
+    lut[s] = pow_n(cos(g * (double)s), N);
+}
+
+template <typename FT, typename OT>
+__global__ void __launch_bounds__(256) dual_lut_kernel(
+    const FT* __restrict__ f, int64_t H, int64_t W, int64_t ld, int64_t out_lo, int64_t out_hi,
+    int S, const double* __restrict__ Wr, const double* __restrict__ Wc,
+    const double* __restrict__ lut, OT* __restrict__ out, unsigned long long* __restrict__ fallback) {
+  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t yo = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
+  const int64_t y = out_lo + yo;
+  bool bad = false;
+  if (x < W && y < out_hi) {
+    const int T = 2 * S + 1;
+    const FT fx = f[y * ld + x];
+    const double* wr = Wr + yo * T;
+    const double* wc = Wc + x * T;
+    const int dy_lo = (int)smax<int64_t>(-S, -y), dy_hi = (int)smin<int64_t>(S, H - 1 - y);
+    const int dx_lo = (int)smax<int64_t>(-S, -x), dx_hi = (int)smin<int64_t>(S, W - 1 - x);
+    double num = 0.0, den = 0.0;
+    for (int dy = dy_lo; dy <= dy_hi; ++dy) {
+      const double a = wr[dy + S];
+      if (a == 0.0) continue;
+      const FT* frow = f + (y + dy) * ld + x;
+      double rn = 0.0, rd = 0.0;
+#pragma unroll 4
+      for (int dx = dx_lo; dx <= dx_hi; ++dx) {
+        const FT v = frow[dx];
+        const int sd = (int)(v - fx);  // exact: integer samples below 2^24
+        const double w = wc[dx + S] * __ldg(lut + (sd < 0 ? -sd : sd));
+        rn = fma(w, (double)v, rn);
+        rd += w;
+      }
+      num = fma(a, rn, num);
+      den = fma(a, rd, den);
+    }
+    bad = !(den > 0.0);  // bilateral.py:244
+    out[yo * W + x] = (OT)(bad ? (double)fx : num / den);
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(fallback, (unsigned long long)__popc(m));
+}
+
+// Row i of the 1-D effective smoothing matrix on an axis of length n:
+// A = B^passes with B[k][j] = w(|k-j|) / cnt(k) (w = 1 inside the radius,
+// alpha at r+1, samples outside the axis dropped), written as weights of
+// samples i-S .. i+S.
+void axis_row(int64_t n, int64_t i, int r, double alpha, int passes, int S, double* out) {
+  const int T = 2 * S + 1;
+  std::vector<double> u(T, 0.0), v(T, 0.0);
+  u[S] = 1.0;  // index t <-> sample i - S + t
+  const int e = alpha > 0.0 ? r + 1 : r;
+  for (int p = 0; p < passes; ++p) {
+    std::fill(v.begin(), v.end(), 0.0);
+    for (int t = 0; t < T; ++t) {
+      if (u[t] == 0.0) continue;
+      const int64_t k = i - S + t;  // output sample of this pass
+      if (k < 0 || k >= n) continue;
+      double cnt = 0.0;
+      for (int d = -e; d <= e; ++d) {
+        const int64_t j = k + d;
+        if (j < 0 || j >= n) continue;
+        cnt += (d >= -r && d <= r) ? 1.0 : alpha;
+      }
+      for (int d = -e; d <= e; ++d) {
+        const int64_t j = k + d;
+        const int64_t tj = t + d;
+        if (j < 0 || j >= n || tj < 0 || tj >= T) continue;
+        v[tj] += u[t] * ((d >= -r && d <= r) ? 1.0 : alpha) / cnt;
+      }
+    }
+    u.swap(v);
+  }
+  for (int t = 0; t < T; ++t) out[t] = u[t];
+}
+
+}  // namespace
+
+int dual_support(const sbf_spatial& sp) {
+  if (sp.mode == SBF_SPATIAL_BOX) return sp.r;
+  return sp.passes * (sp.r + (sp.alpha > 0.0 ? 1 : 0));
+}
+
+// cost model (measured on B200, fp64): term sweeps ~0.17 ns per pixel-term,
+// dual form ~5.5 ps per pixel-tap with the power, less with the table
+bool dual_preferred(const FilterLaunch& a, const sbf_plan& plan) {
+  if (plan.status != SBF_OK || plan.M != 0 || plan.K_eval < 1) return false;
+  if (a.precision != SBF_PREC_HDR) return false;
+  const double S = dual_support(a.sp);
+  const double taps = (2 * S + 1) * (2 * S + 1);
+  return taps * 5.5e-3 < (double)plan.K_eval * 0.17;
+}
+
+int launch_dual_direct(const FilterLaunch& a, const sbf_plan& plan) {
+  cudaStream_t st = a.stream;
+  const int S = dual_support(a.sp);
+  const int T = 2 * S + 1;
+  const int passes = a.sp.mode == SBF_SPATIAL_BOX ? 1 : a.sp.passes;
+  const double alpha = a.sp.mode == SBF_SPATIAL_BOX ? 0.0 : a.sp.alpha;
+  const int64_t rows_out = a.out_hi - a.out_lo;
+  // the weights of sample j in output i depend on the global axis (row0, img_H)
+  // the interior row is shared by every position at least 2S from both ends
+  std::vector<double> hr((size_t)rows_out * T), hc((size_t)a.W * T);
+  std::vector<double> interior_r(T), interior_c(T);
+  const int64_t mid_r = a.img_H / 2, mid_c = a.W / 2;
+  axis_row(a.img_H, mid_r, a.sp.r, alpha, passes, S, interior_r.data());
+  axis_row(a.W, mid_c, a.sp.r, alpha, passes, S, interior_c.data());
+  for (int64_t yo = 0; yo < rows_out; ++yo) {
+    const int64_t g = a.row0 + a.out_lo + yo;
+    if (g >= 2 * S && g < a.img_H - 2 * S)
+      std::copy(interior_r.begin(), interior_r.end(), hr.begin() + yo * T);
+    else
+      axis_row(a.img_H, g, a.sp.r, alpha, passes, S, hr.data() + yo * T);
+  }
+  for (int64_t x = 0; x < a.W; ++x) {
+    if (x >= 2 * S && x < a.W - 2 * S)
+      std::copy(interior_c.begin(), interior_c.end(), hc.begin() + x * T);
+    else
+      axis_row(a.W, x, a.sp.r, alpha, passes, S, hc.data() + x * T);
+  }
+  double *Wr = nullptr, *Wc = nullptr;
+  double2* P = nullptr;
+  SBF_CHECK_CUDA(cudaMallocAsync(&Wr, sizeof(double) * hr.size(), st));
+  SBF_CHECK_CUDA(cudaMallocAsync(&Wc, sizeof(double) * hc.size(), st));
+  SBF_CHECK_CUDA(cudaMemcpyAsync(Wr, hr.data(), sizeof(double) * hr.size(),
+                                 cudaMemcpyHostToDevice, st));
+  SBF_CHECK_CUDA(cudaMemcpyAsync(Wc, hc.data(), sizeof(double) * hc.size(),
+                                 cudaMemcpyHostToDevice, st));
+  // pageable sources: the copies above are staged before cudaMemcpyAsync returns
+  const unsigned gpix = (unsigned)smin<int64_t>((a.H * a.W + 255) / 256, 148 * 16);
+  const dim3 tb(32, 8), grid((unsigned)((a.W + 31) / 32), (unsigned)((rows_out + 7) / 8));
+
+  // integer-valued image with a modest range: tabulated kernel
+  int* flag = nullptr;
+  SBF_CHECK_CUDA(cudaMallocAsync(&flag, sizeof(int), st));
+  SBF_CHECK_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  if (a.dtype == SBF_F32)
+    integral_check<float><<<gpix, 256, 0, st>>>(static_cast<const float*>(a.f), a.H, a.W, a.ld, flag);
+  else
+    integral_check<double><<<gpix, 256, 0, st>>>(static_cast<const double*>(a.f), a.H, a.W, a.ld,
+                                                  flag);
+  SBF_CHECK_LAUNCH();
+  int non_integer = 1;
+  double st_host[8];
+  SBF_CHECK_CUDA(cudaMemcpyAsync(&non_integer, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SBF_CHECK_CUDA(cudaMemcpyAsync(st_host, a.stats, sizeof(st_host), cudaMemcpyDeviceToHost, st));
+  SBF_CHECK_CUDA(cudaStreamSynchronize(st));
+  SBF_CHECK_CUDA(cudaFreeAsync(flag, st));
+  const double span = st_host[2] - st_host[1];
+  if (!non_integer && span >= 0.0 && span <= 4194304.0) {
+    const int64_t smax_v = (int64_t)span;
+    double* lut = nullptr;
+    SBF_CHECK_CUDA(cudaMallocAsync(&lut, sizeof(double) * (smax_v + 1), st));
+    kernel_table<<<(unsigned)smin<int64_t>((smax_v + 256) / 256, 148 * 8), 256, 0, st>>>(
+        a.plan, smax_v, lut);
+#define SBF_DUAL_LUT(FT, OT)                                                                     \
+  dual_lut_kernel<FT, OT><<<grid, tb, 0, st>>>(static_cast<const FT*>(a.f), a.H, a.W, a.ld,      \
+                                               a.out_lo, a.out_hi, S, Wr, Wc, lut,               \
+                                               static_cast<OT*>(a.out), a.fallback)
+    if (a.dtype == SBF_F32 && a.out_dtype == SBF_F32) SBF_DUAL_LUT(float, float);
+    else if (a.dtype == SBF_F32) SBF_DUAL_LUT(float, double);
+    else if (a.out_dtype == SBF_F32) SBF_DUAL_LUT(double, float);
+    else SBF_DUAL_LUT(double, double);
+#undef SBF_DUAL_LUT
+    SBF_CHECK_LAUNCH();
+    SBF_CHECK_CUDA(cudaFreeAsync(lut, st));
+    SBF_CHECK_CUDA(cudaFreeAsync(Wr, st));
+    SBF_CHECK_CUDA(cudaFreeAsync(Wc, st));
+    return SBF_OK;
+  }
+  SBF_CHECK_CUDA(cudaMallocAsync(&P, sizeof(double2) * a.H * a.W, st));
+#define SBF_DUAL(FT, OT)                                                                         \
+  do {                                                                                           \
+    phasor_kernel<FT><<<gpix, 256, 0, st>>>(static_cast<const FT*>(a.f), a.H, a.W, a.ld, a.plan, \
+                                            P);                                                  \
+    dual_kernel<FT, OT><<<grid, tb, 0, st>>>(static_cast<const FT*>(a.f), a.H, a.W, a.ld,        \
+                                             a.out_lo, a.out_hi, S, Wr, Wc, P, a.plan,           \
+                                             static_cast<OT*>(a.out), a.fallback);               \
+  } while (0)
+  if (a.dtype == SBF_F32 && a.out_dtype == SBF_F32) SBF_DUAL(float, float);
+  else if (a.dtype == SBF_F32) SBF_DUAL(float, double);
+  else if (a.out_dtype == SBF_F32) SBF_DUAL(double, float);
+  else SBF_DUAL(double, double);
+#undef SBF_DUAL
+  SBF_CHECK_LAUNCH();
+  SBF_CHECK_CUDA(cudaFreeAsync(Wr, st));
+  SBF_CHECK_CUDA(cudaFreeAsync(Wc, st));
+  SBF_CHECK_CUDA(cudaFreeAsync(P, st));
+  return SBF_OK;
+}
+
+}  // namespace sbf

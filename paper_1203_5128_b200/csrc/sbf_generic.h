@@ -26,4 +26,9 @@ struct PlaneSmoother {
   void release(cudaStream_t st);
 };
 
+// Dual (direct) evaluation for untruncated plans (sbf_dual.cu): picked for
+// fp64 filtering when (2S+1)^2 taps per pixel cost less than K terms.
+bool dual_preferred(const FilterLaunch& a, const sbf_plan& plan);
+int launch_dual_direct(const FilterLaunch& a, const sbf_plan& plan);
+
 }  // namespace sbf

@@ -307,3 +307,38 @@ def test_coarse_nlm_budgets():
                                P.IteratedBox(2.0), 4, 0.0, term_budget=10)
     with pytest.raises(P.InvalidParameterError):
         P.PatchSpec(((1, 0),), (10.0,))
+
+
+@pytest.mark.parametrize("shape,spatial,integer", [
+    ((96, 80), None, False), ((37, 130), None, True), ((9, 9), None, False),
+    ((64, 64), ("box", 3), True), ((50, 61), ("iter", 2.5, 2), False),
+    ((70, 33), ("iter", 2.5, 2), True)])
+def test_dual_form_matches_term_sweeps_and_oracle(shape, spatial, integer):
+    """HDR plans with M = 0: the dual evaluation cos(gamma s)^N over the window
+    (tabulated for integer-valued images, powered otherwise) equals the K-term
+    sweeps and the oracle."""
+    lib = _lib.load()
+    img = np.random.default_rng(sum(shape)).uniform(0, 65535, shape)
+    img[: shape[0] // 2] *= 0.1  # two intensity regions
+    if integer:
+        img = np.round(img)
+    if spatial is None:
+        sp, osp = None, None
+    elif spatial[0] == "box":
+        sp, osp = P.Box(spatial[1]), ("box", spatial[1])
+    else:
+        sp, osp = P.IteratedBox(spatial[1], spatial[2]), ("iterated", spatial[1], spatial[2])
+    params = P.FilterParams(sigma_s=3.0, sigma_r=2000.0, epsilon=0.01, spatial=sp)
+    ref = O.shiftable_bf(img, 3.0, 2000.0, 0.01, spatial=osp)
+    assert ref["M"] == 0
+    outs = []
+    try:
+        for mode in (0, 2):
+            assert lib.sbf_set_fp64_method(mode) == 0
+            res = P.shiftable_bf(img, params)
+            assert (res.plan.N, res.plan.M) == (ref["N"], ref["M"])
+            assert_close_image(res.image, ref["image"])
+            outs.append(res.image)
+    finally:
+        lib.sbf_set_fp64_method(1)
+    assert float(np.abs(outs[0] - outs[1]).max()) < 1e-6
