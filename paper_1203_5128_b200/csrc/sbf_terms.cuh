@@ -311,6 +311,10 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
     cp_async_wait<0>();  // previous term's tail copies landed before slots are reused
 #pragma unroll
     for (int j = 0; j < L; ++j) fetch_async(j, j);
+    // the sample of step t is read from the ring one step early (step t-1),
+    // so its shared-memory latency hides behind a whole step of work
+    cp_async_wait<L - 1>();
+    float fnext = fr[0];
 
     for (int t0 = 0; t0 < T_total; t0 += ROWS) {
       const int t1 = min(t0 + ROWS, T_total);
@@ -328,8 +332,9 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
           constexpr int J = decltype(jc)::value;
           const int t = base + J;
           if (KIND >= 1 && (unsigned)(t - t0) >= (unsigned)(t1 - t0)) return;
-          cp_async_wait<L - 1>();
-          const float fc = fr[J] - centerf;
+          const float fc = fnext - centerf;
+          cp_async_wait<L - 2>();  // group of step t+1 has landed
+          fnext = fr[(J + 1) % L];
           // phasor of this pixel for the current term
           const float u = fc * nu;
           const float tt = u - ((u + 12582912.f) - 12582912.f);  // frac, |u| < 2^22
@@ -419,6 +424,16 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
           auto hblock = [&](auto kind_tag, const int base) {
             constexpr int KIND = decltype(kind_tag)::value;
             constexpr bool GUARD = KIND >= 2, BORDER = KIND == 3;
+            // the block's output phasors are read before any VB store: RAW and
+            // VB are disjoint, but the compiler cannot prove it and would
+            // otherwise serialise each load behind the previous store
+            float rw[L];
+            static_for<L>([&](auto jc) {
+              constexpr int J = decltype(jc)::value;
+              const int qq = base + J;
+              if (KIND == 1) rw[J] = rrow[2 * qq];
+              else if (KIND != 0) rw[J] = (qq >= 2 * HALO && qq < HALO_W) ? rrow[2 * qq] : 0.f;
+            });
             static_for<L>([&](auto jc) {
               constexpr int J = decltype(jc)::value;
               const int qq = base + J;
@@ -429,7 +444,7 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
                 x = (c >= 0 && c < p.W) ? x : 0.f;
               }
               const float yv = cascade<J, L, D, PASSES, BORDER>(hd, hlast, x, a, b, gh + qq + GOFF);
-              if (KIND == 1 || (GUARD && qq >= 2 * HALO)) vrow[4 * (qq - HALO)] = yv * rrow[2 * qq];
+              if (KIND == 1 || (GUARD && qq >= 2 * HALO)) vrow[4 * (qq - HALO)] = yv * rw[J];
             });
           };
           for (int kb = 0; kb < NB; ++kb) {
