@@ -468,25 +468,21 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
         const int vlo = max(t0, 2 * HALO) - t0;
         const int vhi = min(t1, 2 * HALO + Bn) - t0;
         const int xlim = min(WC, p.W - strip * WC);  // columns of this strip inside the image
-        constexpr int DV = THREADS / WC, DJ = THREADS % WC;
-        int vv = vlo + tid / WC, j = tid % WC;
-        float2* ndrow = reinterpret_cast<float2*>(p.nd) +
-                        (int64_t)(y0 - 2 * HALO + t0 - p.out_lo) * p.W + strip * WC;
+        // one thread per output column walks the chunk's rows: no index
+        // arithmetic per pixel (constant strides), loads hoisted by unrolling
+        if (tid < xlim) {
+          const float* vb = VB + vlo * VBP + 4 * (HALO + tid);
+          float2* dst = reinterpret_cast<float2*>(p.nd) +
+                        (int64_t)(y0 - 2 * HALO + t0 + vlo - p.out_lo) * p.W + strip * WC + tid;
 #pragma unroll 4
-        for (; vv < vhi;) {
-          if (j < xlim) {
-            const float4 pv = *reinterpret_cast<const float4*>(VB + vv * VBP + 4 * (HALO + j));
+          for (int vv = vlo; vv < vhi; ++vv) {
+            const float4 pv = *reinterpret_cast<const float4*>(vb);
+            vb += VBP;
             // the term weight is applied once per output pixel here
             const float num = scale * ((IMGS == 4) ? pv.x + pv.y : pv.x + pv.z);
             const float den = scale * ((IMGS == 4) ? pv.z + pv.w : pv.y + pv.w);
-            float2* dst = ndrow + (int64_t)vv * p.W + j;
             asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dst), "f"(num), "f"(den));
-          }
-          vv += DV;
-          j += DJ;
-          if (j >= WC) {
-            j -= WC;
-            ++vv;
+            dst += p.W;
           }
         }
       }
