@@ -18,6 +18,7 @@ Prints exactly one JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import multiprocessing as mp
 import os
@@ -286,9 +287,14 @@ def run_ours(args, rank, world, dev):
 
     # e2e through the public API from pinned host memory (input H2D + result D2H)
     pinned = torch.from_numpy(np.ascontiguousarray(img_np)).pin_memory()
-    for _ in range(max(1, args.warmup)):
-        P.shiftable_bf(pinned, params)
+    res = None
+    for _ in range(max(3, args.warmup)):
+        # keep the previous result alive exactly like the timed loop, so the
+        # pinned-host caching allocator holds both result blocks before timing
+        res = P.shiftable_bf(pinned, params)
     torch.cuda.synchronize()
+    gc.collect()
+    gc.disable()  # no collector pauses inside the timed region
     e2e_ms = []
     for _ in range(args.steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -298,6 +304,7 @@ def run_ours(args, rank, world, dev):
         e1.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
         flush.zero_()
+    gc.enable()
     e2e_total = float(np.sum(e2e_ms))
     if world > 1:
         t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
