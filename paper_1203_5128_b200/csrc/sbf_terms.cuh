@@ -447,17 +447,38 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
               if (KIND == 1 || (GUARD && qq >= 2 * HALO)) vrow[4 * (qq - HALO)] = yv * rw[J];
             });
           };
-          for (int kb = 0; kb < NB; ++kb) {
-            const int base = kb * L;
-            const bool gin = base - (PASSES + 2) * D - 1 >= qg_lo && base + L - 1 <= qg_hi;
-            if (gin && base + L <= 2 * HALO)
-              hblock(std::integral_constant<int, 0>{}, base);
-            else if (gin && base >= 2 * HALO && base + L <= HALO_W)
-              hblock(std::integral_constant<int, 1>{}, base);
-            else if (gin)
-              hblock(std::integral_constant<int, 2>{}, base);
-            else
-              hblock(std::integral_constant<int, 3>{}, base);
+          // interior strips (no column touches an image border) run a fixed
+          // block sequence: warm-up blocks, one guarded block, a loop of main
+          // blocks, guarded tail — no per-block variant dispatch
+          constexpr int KB_MAIN0 = (2 * HALO + L - 1) / L;  // first block with base >= 2*HALO
+          constexpr int KB_MAIN1 = (HALO_W - L) / L + 1;    // blocks [KB_MAIN0, KB_MAIN1) are main
+          const bool strip_in = -(PASSES + 2) * D - 1 >= qg_lo && NB * L - 1 <= qg_hi;
+          if (strip_in && KB_MAIN0 < KB_MAIN1) {
+            static_for<KB_MAIN0>([&](auto kc) {
+              constexpr int KB = decltype(kc)::value;
+              if constexpr (KB * L + L <= 2 * HALO)
+                hblock(std::integral_constant<int, 0>{}, KB * L);
+              else
+                hblock(std::integral_constant<int, 2>{}, KB * L);
+            });
+#pragma unroll 1
+            for (int kb = KB_MAIN0; kb < KB_MAIN1; ++kb) hblock(std::integral_constant<int, 1>{}, kb * L);
+            static_for<NB - KB_MAIN1>([&](auto kc) {
+              hblock(std::integral_constant<int, 2>{}, (KB_MAIN1 + decltype(kc)::value) * L);
+            });
+          } else {
+            for (int kb = 0; kb < NB; ++kb) {
+              const int base = kb * L;
+              const bool gin = base - (PASSES + 2) * D - 1 >= qg_lo && base + L - 1 <= qg_hi;
+              if (gin && base + L <= 2 * HALO)
+                hblock(std::integral_constant<int, 0>{}, base);
+              else if (gin && base >= 2 * HALO && base + L <= HALO_W)
+                hblock(std::integral_constant<int, 1>{}, base);
+              else if (gin)
+                hblock(std::integral_constant<int, 2>{}, base);
+              else
+                hblock(std::integral_constant<int, 3>{}, base);
+            }
           }
         }
       }
