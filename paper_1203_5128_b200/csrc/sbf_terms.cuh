@@ -62,6 +62,9 @@ struct TermParams {
   int64_t nd_group_stride;  // (num, den) pairs per group
 };
 
+#ifndef SBF_V_MAIN_VARIANT
+#define SBF_V_MAIN_VARIANT 0  // separate unchecked V block variant for whole blocks (bigger code: slower)
+#endif
 #ifndef SBF_IMGS4_MAX_R
 #define SBF_IMGS4_MAX_R 4  // radii up to this run 4 images per V thread
 #endif
@@ -396,9 +399,12 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
         const bool clean = base >= 2 * HALO && base + L <= HALO + Bn &&
                            base + 2 * L - 1 <= sf_hi &&
                            base - (PASSES + 2) * D - 1 >= sg_lo && base + L - 1 <= sg_hi;
+#if SBF_V_MAIN_VARIANT
         if (clean && base >= t0 && base + L <= t1)
           vblock(std::integral_constant<int, 0>{}, base);
-        else if (clean)
+        else
+#endif
+        if (clean)
           vblock(std::integral_constant<int, 1>{}, base);
         else
           vblock(std::integral_constant<int, 2>{}, base);
