@@ -433,13 +433,17 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
             // the block's output phasors are read before any VB store: RAW and
             // VB are disjoint, but the compiler cannot prove it and would
             // otherwise serialise each load behind the previous store
-            float rw[L];
-            static_for<L>([&](auto jc) {
-              constexpr int J = decltype(jc)::value;
-              const int qq = base + J;
-              if (KIND == 1) rw[J] = rrow[2 * qq];
-              else if (KIND != 0) rw[J] = (qq >= 2 * HALO && qq < HALO_W) ? rrow[2 * qq] : 0.f;
-            });
+            // (long rings, r > 5: loaded at use, the registers are needed elsewhere)
+            constexpr bool PREF = L <= 13;
+            float rw[PREF ? L : 1];
+            if constexpr (PREF) {
+              static_for<L>([&](auto jc) {
+                constexpr int J = decltype(jc)::value;
+                const int qq = base + J;
+                if (KIND == 1) rw[J] = rrow[2 * qq];
+                else if (KIND != 0) rw[J] = (qq >= 2 * HALO && qq < HALO_W) ? rrow[2 * qq] : 0.f;
+              });
+            }
             static_for<L>([&](auto jc) {
               constexpr int J = decltype(jc)::value;
               const int qq = base + J;
@@ -450,7 +454,8 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
                 x = (c >= 0 && c < p.W) ? x : 0.f;
               }
               const float yv = cascade<J, L, D, PASSES, BORDER>(hd, hlast, x, a, b, gh + qq + GOFF);
-              if (KIND == 1 || (GUARD && qq >= 2 * HALO)) vrow[4 * (qq - HALO)] = yv * rw[J];
+              if (KIND == 1 || (GUARD && qq >= 2 * HALO))
+                vrow[4 * (qq - HALO)] = yv * (PREF ? rw[PREF ? J : 0] : rrow[2 * qq]);
             });
           };
           // interior strips (no column touches an image border) run a fixed
@@ -495,21 +500,24 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
         const int vlo = max(t0, 2 * HALO) - t0;
         const int vhi = min(t1, 2 * HALO + Bn) - t0;
         const int xlim = min(WC, p.W - strip * WC);  // columns of this strip inside the image
-        // one thread per output column walks the chunk's rows: no index
-        // arithmetic per pixel (constant strides), loads hoisted by unrolling
-        if (tid < xlim) {
-          const float* vb = VB + vlo * VBP + 4 * (HALO + tid);
+        // G groups of one thread per output column walk every G-th row of
+        // the chunk: no index arithmetic per pixel (constant strides)
+        constexpr int G = THREADS / WC;
+        const int jc = tid % WC, g = tid / WC;
+        if (g < G && jc < xlim) {
+          const float* vb = VB + (vlo + g) * VBP + 4 * (HALO + jc);
           float2* dst = reinterpret_cast<float2*>(p.nd) +
-                        (int64_t)(y0 - 2 * HALO + t0 + vlo - p.out_lo) * p.W + strip * WC + tid;
+                        (int64_t)(y0 - 2 * HALO + t0 + vlo + g - p.out_lo) * p.W + strip * WC + jc;
+          const int64_t dstride = (int64_t)G * p.W;
 #pragma unroll 4
-          for (int vv = vlo; vv < vhi; ++vv) {
+          for (int vv = vlo + g; vv < vhi; vv += G) {
             const float4 pv = *reinterpret_cast<const float4*>(vb);
-            vb += VBP;
+            vb += G * VBP;
             // the term weight is applied once per output pixel here
             const float num = scale * ((IMGS == 4) ? pv.x + pv.y : pv.x + pv.z);
             const float den = scale * ((IMGS == 4) ? pv.z + pv.w : pv.y + pv.w);
             asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dst), "f"(num), "f"(den));
-            dst += p.W;
+            dst += dstride;
           }
         }
       }
