@@ -65,6 +65,9 @@ struct TermParams {
 #ifndef SBF_V_MAIN_VARIANT
 #define SBF_V_MAIN_VARIANT 0  // separate unchecked V block variant for whole blocks (bigger code: slower)
 #endif
+#ifndef SBF_H_FIXED_SEQ
+#define SBF_H_FIXED_SEQ 1  // interior strips: warm-up / main-loop / tail H blocks, no dispatch
+#endif
 #ifndef SBF_IMGS4_MAX_R
 #define SBF_IMGS4_MAX_R 4  // radii up to this run 4 images per V thread
 #endif
@@ -464,7 +467,7 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
           constexpr int KB_MAIN0 = (2 * HALO + L - 1) / L;  // first block with base >= 2*HALO
           constexpr int KB_MAIN1 = (HALO_W - L) / L + 1;    // blocks [KB_MAIN0, KB_MAIN1) are main
           const bool strip_in = -(PASSES + 2) * D - 1 >= qg_lo && NB * L - 1 <= qg_hi;
-          if (strip_in && KB_MAIN0 < KB_MAIN1) {
+          if (SBF_H_FIXED_SEQ && strip_in && KB_MAIN0 < KB_MAIN1) {
             static_for<KB_MAIN0>([&](auto kc) {
               constexpr int KB = decltype(kc)::value;
               if constexpr (KB * L + L <= 2 * HALO)
