@@ -65,6 +65,9 @@ struct TermParams {
 #ifndef SBF_V_MAIN_VARIANT
 #define SBF_V_MAIN_VARIANT 0  // separate unchecked V block variant for whole blocks (bigger code: slower)
 #endif
+#ifndef SBF_F_EARLY
+#define SBF_F_EARLY 1  // read the next step's sample one step early
+#endif
 #ifndef SBF_H_FIXED_SEQ
 #define SBF_H_FIXED_SEQ 1  // interior strips: warm-up / main-loop / tail H blocks, no dispatch
 #endif
@@ -338,9 +341,14 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
           constexpr int J = decltype(jc)::value;
           const int t = base + J;
           if (KIND >= 1 && (unsigned)(t - t0) >= (unsigned)(t1 - t0)) return;
+#if SBF_F_EARLY
           const float fc = fnext - centerf;
           cp_async_wait<L - 2>();  // group of step t+1 has landed
           fnext = fr[(J + 1) % L];
+#else
+          cp_async_wait<L - 1>();
+          const float fc = fr[J] - centerf;
+#endif
           // phasor of this pixel for the current term
           const float u = fc * nu;
           const float tt = u - ((u + 12582912.f) - 12582912.f);  // frac, |u| < 2^22
