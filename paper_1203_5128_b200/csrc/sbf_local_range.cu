@@ -64,6 +64,18 @@ __global__ void __launch_bounds__(256) rowmax_kernel(const T* __restrict__ f, in
   for (int j = threadIdx.x; j < nout; j += blockDim.x) orow[j] = vmax(suf[j], q[j + 2 * R]);
 }
 
+__device__ __forceinline__ void finalize_stats(double* stats) {
+  const unsigned long long* red = reinterpret_cast<const unsigned long long*>(stats + 4);
+  const double T = ord_value(red[0]);
+  const double mn = ord_value(red[1]), mx = ord_value(red[2]);
+  stats[0] = T;
+  stats[1] = mn;
+  stats[2] = mx;
+  // centre used by the term kernel: any constant works (BF(f + c) = BF(f) + c);
+  // mid-range rounded to fp32 halves the magnitudes the fp32 sums carry.
+  stats[3] = (isfinite(mn) && isfinite(mx)) ? (double)(float)(0.5 * (mn + mx)) : 0.0;
+}
+
 template <typename T>
 __device__ __forceinline__ double block_reduce(double v, bool is_max, double* red) {
   for (int o = 16; o; o >>= 1) {
@@ -90,7 +102,8 @@ __device__ __forceinline__ double block_reduce(double v, bool is_max, double* re
 template <typename T>
 __global__ void __launch_bounds__(kColTile* kColThreadsY) colmax_kernel(
     const T* __restrict__ rowmax, const T* __restrict__ f, int64_t H, int64_t W, int64_t ld,
-    int R, int64_t t_lo, int64_t t_hi, T* __restrict__ M_out, unsigned long long* __restrict__ red) {
+    int R, int64_t t_lo, int64_t t_hi, T* __restrict__ M_out, unsigned long long* __restrict__ red,
+    unsigned* __restrict__ done) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int win = 2 * R + 1;
   const int64_t y0 = (int64_t)blockIdx.y * kColRows;
@@ -142,14 +155,39 @@ __global__ void __launch_bounds__(kColTile* kColThreadsY) colmax_kernel(
       }
     }
   }
-  tmax = block_reduce<T>(tmax, true, dred);
-  if (tx == 0 && ty == 0) atomicMax(&red[0], ord_bits(tmax));
-  fmn = block_reduce<T>(fmn, false, dred);
-  if (tx == 0 && ty == 0) atomicMin(&red[1], ord_bits(fmn));
-  fmx = block_reduce<T>(fmx, true, dred);
-  if (tx == 0 && ty == 0) atomicMax(&red[2], ord_bits(fmx));
-  for (int o = 16; o; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
-  if (((ty * kColTile + tx) & 31) == 0 && bad) atomicAdd(&red[3], bad);
+  // one combined block reduction of (T, min, max, #non-finite)
+  for (int o = 16; o; o >>= 1) {
+    tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+    fmn = fmin(fmn, __shfl_xor_sync(0xffffffffu, fmn, o));
+    fmx = fmax(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  const int tid = ty * kColTile + tx, lane = tid & 31, warp = tid >> 5;
+  if (lane == 0) {
+    dred[4 * warp] = tmax;
+    dred[4 * warp + 1] = fmn;
+    dred[4 * warp + 2] = fmx;
+    dred[4 * warp + 3] = __longlong_as_double((long long)bad);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < kColTile * kColThreadsY / 32; ++w) {
+      tmax = fmax(tmax, dred[4 * w]);
+      fmn = fmin(fmn, dred[4 * w + 1]);
+      fmx = fmax(fmx, dred[4 * w + 2]);
+      bad += (unsigned long long)__double_as_longlong(dred[4 * w + 3]);
+    }
+    atomicMax(&red[0], ord_bits(tmax));
+    atomicMin(&red[1], ord_bits(fmn));
+    atomicMax(&red[2], ord_bits(fmx));
+    if (bad) atomicAdd(&red[3], bad);
+    // the last CTA folds the atomics into stats (no finalisation launch)
+    __threadfence();
+    if (atomicAdd(done, 1u) == gridDim.x * gridDim.y - 1) {
+      __threadfence();
+      finalize_stats(reinterpret_cast<double*>(red) - 4);
+    }
+  }
 }
 
 // R == 0: T = 0 by definition (maxfilter.py:58-59); statistics only.
@@ -180,7 +218,8 @@ __global__ void stats_only_kernel(const T* __restrict__ f, int64_t W, int64_t ld
   if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&red[3], bad);
 }
 
-__global__ void stats_init_kernel(double* stats) {
+__global__ void stats_init_kernel(double* stats, unsigned* done) {
+  if (done) *done = 0u;
   unsigned long long* red = reinterpret_cast<unsigned long long*>(stats + 4);
   red[0] = ord_bits(0.0);
   red[1] = ord_bits(INFINITY);
@@ -188,16 +227,11 @@ __global__ void stats_init_kernel(double* stats) {
   red[3] = 0ull;  // non-finite sample count (stats[7], read as uint64)
 }
 
-__global__ void stats_final_kernel(double* stats) {
-  const unsigned long long* red = reinterpret_cast<const unsigned long long*>(stats + 4);
-  const double T = ord_value(red[0]);
-  const double mn = ord_value(red[1]), mx = ord_value(red[2]);
-  stats[0] = T;
-  stats[1] = mn;
-  stats[2] = mx;
-  // centre used by the term kernel: any constant works (BF(f + c) = BF(f) + c);
-  // mid-range rounded to fp32 halves the magnitudes the fp32 sums carry.
-  stats[3] = (isfinite(mn) && isfinite(mx)) ? (double)(float)(0.5 * (mn + mx)) : 0.0;
+__global__ void stats_final_kernel(double* stats) { finalize_stats(stats); }
+
+template <typename T>
+size_t local_range_ws_bytes(int64_t H, int64_t W) {
+  return align_up((size_t)(H * W) * sizeof(T)) + 256;  // row-max image + CTA counter
 }
 
 template <typename T>
@@ -205,7 +239,13 @@ int run(const void* fv, int64_t H, int64_t W, int64_t ld, int R, int64_t t_lo, i
         void* M_out, double* stats, void* ws, size_t ws_bytes, cudaStream_t st) {
   const T* f = static_cast<const T*>(fv);
   unsigned long long* red = reinterpret_cast<unsigned long long*>(stats + 4);
-  stats_init_kernel<<<1, 1, 0, st>>>(stats);
+  unsigned* done = nullptr;
+  if (R > 0) {
+    SBF_REQUIRE(ws && ws_bytes >= local_range_ws_bytes<T>(H, W), SBF_ERR_WORKSPACE,
+                "local_range workspace too small");
+    done = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + align_up((size_t)(H * W) * sizeof(T)));
+  }
+  stats_init_kernel<<<1, 1, 0, st>>>(stats, done);
   SBF_CHECK_LAUNCH();
   // a window wider than the image equals the image-wide window (clamping)
   const int Rr = (int)smin<int64_t>(R, smax<int64_t>(W - 1, 0));
@@ -239,9 +279,10 @@ int run(const void* fv, int64_t H, int64_t W, int64_t ld, int R, int64_t t_lo, i
       dim3 grid((unsigned)((W + kColTile - 1) / kColTile), (unsigned)((H + kColRows - 1) / kColRows));
       dim3 block(kColTile, kColThreadsY);
       colmax_kernel<T><<<grid, block, smem, st>>>(rowmax, f, H, W, ld, Rc, t_lo, t_hi,
-                                                  static_cast<T*>(M_out), red);
+                                                  static_cast<T*>(M_out), red, done);
       SBF_CHECK_LAUNCH();
     }
+    return SBF_OK;  // colmax's last CTA wrote the final statistics
   }
   stats_final_kernel<<<1, 1, 0, st>>>(stats);
   SBF_CHECK_LAUNCH();
@@ -251,7 +292,7 @@ int run(const void* fv, int64_t H, int64_t W, int64_t ld, int R, int64_t t_lo, i
 }  // namespace
 
 size_t local_range_ws(int64_t H, int64_t W, int dtype) {
-  return align_up((size_t)(H * W) * (dtype == SBF_F64 ? 8 : 4));
+  return dtype == SBF_F64 ? local_range_ws_bytes<double>(H, W) : local_range_ws_bytes<float>(H, W);
 }
 
 int launch_local_range(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int R,
