@@ -240,6 +240,10 @@ int sbf_nlm_filter(const void* f, int dtype, int64_t H, int64_t W, int64_t ld,
  * 1 = cost model (default: the dual form cos(gamma s)^N over the (2S+1)^2
  * window when M = 0 and it is cheaper), 2 = dual whenever M = 0. */
 int sbf_set_fp64_method(int mode);
+/* fp32 term sweeps, this thread: radii >= r (with an instantiation) run the
+ * split column/row sweep instead of the fused strip kernel K3 (default 9;
+ * 0 = always K3). */
+int sbf_set_split_min_radius(int r);
 int sbf_num_specialisations(void);
 int sbf_specialisation(int i, int* r, int* passes, int* mode);
 int sbf_filter_geometry(int64_t rows_out, int64_t W, const sbf_spatial* sp, int precision,

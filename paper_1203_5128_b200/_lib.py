@@ -82,6 +82,7 @@ _SIGS = {
     "sbf_pgm_encode": (_int, [_vp, _int, _i64, _int, _vp, _vp]),
     "sbf_direct_bf": (_int, [_vp, _int, _i64, _i64, _i64, _int, _vp, _dbl, _int, _vp, _int, _vp]),
     "sbf_set_fp64_method": (_int, [_int]),
+    "sbf_set_split_min_radius": (_int, [_int]),
     "sbf_nlm_filter": (_int, [_vp, _int, _i64, _i64, _i64, C.POINTER(SbfSpatial), _int, _vp, _vp,
                               _int, _vp, _vp, _int, _vp, _vp]),
     "sbf_fp32_probe": (_int, [_int, _int, _int, _vp, _vp]),

@@ -43,6 +43,13 @@ def instantiations(kind: str):
     return out
 
 
+def split_instantiations(kind: str):
+    """(r, passes) pairs with a split-sweep (SV/SH) instantiation."""
+    if kind == "min":
+        return [(5, 3)]
+    return [(r, 3) for r in range(5, 13)]
+
+
 def _newer(target, deps):
     if not os.path.exists(target):
         return False
@@ -83,8 +90,18 @@ def build(kind: str = "full", jobs: int | None = None, verbose: bool = False,
     if not os.path.exists(inc) or open(inc).read() != text:
         with open(inc, "w") as fh:
             fh.write(text)
+    sinst = split_instantiations(kind)
+    sinc = os.path.join(CSRC, "sbf_split_list.inc")
+    stext = "".join(f"SBF_Y({r}, {p})\n" for r, p in sinst)
+    if not os.path.exists(sinc) or open(sinc).read() != stext:
+        with open(sinc, "w") as fh:
+            fh.write(stext)
     jobs_list = [(os.path.join(CSRC, s), os.path.join(obj_dir, s.replace(".cu", ".o")), defs)
                  for s in SOURCES]
+    for r, p in sinst:
+        jobs_list.append((os.path.join(CSRC, "sbf_split_inst.cu"),
+                          os.path.join(obj_dir, f"split_r{r}_p{p}.o"),
+                          defs + [f"-DSBF_R={r}", f"-DSBF_P={p}"]))
     for r, p, m in inst:
         jobs_list.append((os.path.join(CSRC, "sbf_terms_inst.cu"),
                           os.path.join(obj_dir, f"terms_r{r}_p{p}_m{m}.o"),

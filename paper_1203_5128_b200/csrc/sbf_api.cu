@@ -7,6 +7,7 @@
 #include "sbf_common.cuh"
 #include "sbf_plan_logic.cuh"
 #include "sbf_generic.h"
+#include "sbf_split.cuh"
 #include "sbf_terms.cuh"
 
 namespace sbf {
@@ -26,6 +27,28 @@ int launch_generic_terms(const FilterLaunch& a, double* nd);
 #define SBF_X(R, P, M) TermsEntry terms_entry_##R##_##P##_##M();
 #include "sbf_terms_list.inc"
 #undef SBF_X
+
+// ---- registry of split-sweep instantiations (generated list) ----
+#define SBF_Y(R, P) SplitEntry split_entry_##R##_##P();
+#include "sbf_split_list.inc"
+#undef SBF_Y
+
+// radii at or above this use the split sweep when an instantiation exists
+// (fp32 precision); 0 disables the split path
+static thread_local int g_split_min_r = 9;  // measured crossover vs K3 on B200 (r=5..8: K3 faster)
+
+static const SplitEntry* find_split(const sbf_spatial& sp, int precision) {
+  static const std::vector<SplitEntry> reg = {
+#define SBF_Y(R, P) split_entry_##R##_##P(),
+#include "sbf_split_list.inc"
+#undef SBF_Y
+  };
+  if (precision != SBF_PREC_FP32 || g_split_min_r <= 0 || sp.mode == SBF_SPATIAL_BOX) return nullptr;
+  if (sp.r < g_split_min_r || !(sp.alpha <= 0.999)) return nullptr;
+  for (const auto& e : reg)
+    if (e.r == sp.r && e.passes == sp.passes) return &e;
+  return nullptr;
+}
 
 static const std::vector<TermsEntry>& registry() {
   static const std::vector<TermsEntry> reg = {
@@ -89,6 +112,12 @@ static bool spatial_coeffs(const sbf_spatial& sp, int* r, int* passes, double* a
 // partial accumulators (+ an fp32 centred copy of float64 inputs for K3)
 size_t filter_ws(int64_t H, int64_t W, int64_t rows_out, int dtype, const sbf_spatial* sp,
                  int precision) {
+  if (find_split(*sp, precision)) {
+    // split sweep: accumulator + column-smoothed images of one term
+    size_t bytes = align_up((size_t)(rows_out * W) * 8) + align_up((size_t)(rows_out * W) * 16);
+    if (dtype == SBF_F64) bytes += align_up((size_t)(H * W) * 4);
+    return bytes;
+  }
   const TermsEntry* e = find_entry(*sp, precision);
   if (!e) return align_up((size_t)(rows_out * W) * 16);  // generic: one fp64 accumulator
   TermGeom g;
@@ -161,6 +190,73 @@ static thread_local int g_stage_mask = 3;
 // whenever exact (M = 0)
 static thread_local int g_dual_mode = 1;
 
+// fp32 input view for the term kernels: fp64 inputs get a centred fp32 copy
+static const float* f32_view(const FilterLaunch& a, void* scratch, int64_t* ld, int* centred) {
+  if (a.dtype != SBF_F64) {
+    *ld = a.ld;
+    *centred = 0;
+    return static_cast<const float*>(a.f);
+  }
+  float* fc = static_cast<float*>(scratch);
+  const unsigned grid = (unsigned)smin<int64_t>((a.H * a.W + 255) / 256, 148 * 8);
+  centre_to_f32_kernel<<<grid, 256, 0, a.stream>>>(static_cast<const double*>(a.f), a.H, a.W, a.ld,
+                                                   a.stats, fc);
+  *ld = a.W;
+  *centred = 1;
+  return fc;
+}
+
+// split sweep (r >= g_split_min_r): SV + SH per term, then K4
+static int launch_split_path(const FilterLaunch& a, const SplitEntry& se, int r, double alpha) {
+  const int64_t rows_out = a.out_hi - a.out_lo;
+  const size_t nd_bytes = align_up((size_t)(rows_out * a.W) * 8);
+  const size_t u_bytes = align_up((size_t)(rows_out * a.W) * 16);
+  const size_t need = filter_ws(a.H, a.W, rows_out, a.dtype, &a.sp, a.precision);
+  SBF_REQUIRE(a.ws && a.ws_bytes >= need, SBF_ERR_WORKSPACE,
+              "filter workspace too small (%zu < %zu)", a.ws_bytes, need);
+  char* ws = static_cast<char*>(a.ws);
+  SplitParams p;
+  memset(&p, 0, sizeof(p));
+  p.f = f32_view(a, ws + nd_bytes + u_bytes, &p.ld, &p.centred);
+  p.H = (int)a.H;
+  p.W = (int)a.W;
+  p.row0 = a.row0;
+  p.img_H = a.img_H;
+  p.out_lo = (int)a.out_lo;
+  p.out_hi = (int)a.out_hi;
+  p.r = r;
+  p.alpha = (float)alpha;
+  const double cint = 2.0 * r + 1.0 + 2.0 * alpha;
+  p.a = (float)((1.0 - alpha) / cint);
+  p.b = (float)(alpha / cint);
+  p.plan = a.plan;
+  p.terms = a.terms;
+  p.stats = a.stats;
+  p.nd = reinterpret_cast<float2*>(ws);
+  p.U = reinterpret_cast<float*>(ws + nd_bytes);
+  // geometry: >= 4 CTAs per SM for both kernels, halos <= 1/8 of the work
+  const int halo = se.passes * (r + 1);
+  const int64_t sv_cols = (r <= 4) ? 128 : 64;
+  const int64_t cgroups = (a.W + sv_cols - 1) / sv_cols;
+  const int64_t want = 4 * 148;
+  const int64_t nb = smax<int64_t>(1, (want + cgroups - 1) / cgroups);
+  p.band = (int)smin<int64_t>(smax<int64_t>(8 * halo, (rows_out + nb - 1) / nb), 1024);
+  const int64_t rgroups = (rows_out + 31) / 32;
+  const int64_t ns = smax<int64_t>(1, (want + rgroups - 1) / rgroups);
+  p.seg = (int)smax<int64_t>(16 * halo, (a.W + ns - 1) / ns);
+  sbf_plan plan;
+  SBF_CHECK_CUDA(cudaMemcpyAsync(&plan, a.plan, sizeof(plan), cudaMemcpyDeviceToHost, a.stream));
+  SBF_CHECK_CUDA(cudaStreamSynchronize(a.stream));
+  const int K = plan.status == SBF_OK ? plan.K_eval : 0;
+  if (g_stage_mask & 1) {
+    if (K == 0) SBF_CHECK_CUDA(cudaMemsetAsync(p.nd, 0, nd_bytes, a.stream));
+    int rc = se.launch(p, K, a.stream);
+    if (rc != SBF_OK) return rc;
+  }
+  if (!(g_stage_mask & 2)) return SBF_OK;
+  return launch_epilogue<float>(a, reinterpret_cast<const float*>(p.nd), 1, rows_out * a.W);
+}
+
 int launch_filter(const FilterLaunch& a) {
   int r, passes;
   double alpha;
@@ -183,6 +279,7 @@ int launch_filter(const FilterLaunch& a) {
   const int64_t rows_out = a.out_hi - a.out_lo;
   SBF_REQUIRE(a.H <= INT32_MAX && a.W <= INT32_MAX, SBF_ERR_INVALID, "image too large");
 
+  if (const SplitEntry* se = find_split(a.sp, a.precision)) return launch_split_path(a, *se, r, alpha);
   const TermsEntry* e = find_entry(a.sp, a.precision);
   if (!e) {
     const size_t need = align_up((size_t)(rows_out * a.W) * 16);
@@ -271,6 +368,12 @@ int sbf_abi_version(void) { return SBF_ABI_VERSION; }
 int sbf_set_stage_mask(int mask) {
   if (mask < 1 || mask > 3) return SBF_ERR_INVALID;
   sbf::g_stage_mask = mask;
+  return SBF_OK;
+}
+
+int sbf_set_split_min_radius(int r) {
+  if (r < 0) return SBF_ERR_INVALID;
+  sbf::g_split_min_r = r;
   return SBF_OK;
 }
 

@@ -342,3 +342,25 @@ def test_dual_form_matches_term_sweeps_and_oracle(shape, spatial, integer):
     finally:
         lib.sbf_set_fp64_method(1)
     assert float(np.abs(outs[0] - outs[1]).max()) < 1e-6
+
+
+@pytest.mark.parametrize("shape,sigma_s,sigma_r", [((300, 257), 6.0, 20.0), ((97, 515), 12.0, 15.0),
+                                                   ((64, 64), 8.0, 30.0), ((333, 90), 10.0, 25.0)])
+def test_split_sweep_matches_strip_kernel_and_oracle(shape, sigma_s, sigma_r):
+    """Radii >= 5 run the split column/row sweep; it must agree with the fused
+    strip kernel (forced via sbf_set_split_min_radius(0)) and the oracle."""
+    lib = _lib.load()
+    img = np.random.default_rng(shape[1]).uniform(0, 255, shape).astype(np.float32)
+    params = P.FilterParams(sigma_s=sigma_s, sigma_r=sigma_r, epsilon=0.01)
+    ref = O.shiftable_bf(img, sigma_s, sigma_r, 0.01)
+    outs = []
+    try:
+        for mode in (1, 0):  # split sweep forced for any instantiated radius, then K3
+            assert lib.sbf_set_split_min_radius(mode) == 0
+            res = P.shiftable_bf(img, params)
+            assert (res.plan.N, res.plan.M) == (ref["N"], ref["M"])
+            assert_close_image(res.image, ref["image"])
+            outs.append(res.image)
+    finally:
+        lib.sbf_set_split_min_radius(9)
+    assert float(np.abs(outs[0] - outs[1]).max()) < 5e-3
