@@ -256,11 +256,17 @@ __global__ void __launch_bounds__(128) sh_kernel(const SplitParams p) {
     constexpr int KIND = decltype(kind_tag)::value;
     constexpr bool GUARD = KIND >= 2, BORDER = KIND == 3;
     const int rb = (base - s0) % RINGC;  // blocks never wrap: RINGC is a multiple of L
+    // inputs are read two steps ahead: the in-place output stores use a
+    // wrapped (runtime) index, so the compiler cannot move later loads above
+    // them; issuing each load two steps early hides its latency anyway
+    float xa = lrow[4 * rb], xb = lrow[4 * (rb + 1)];
     static_for<L>([&](auto jc) {
       constexpr int J = decltype(jc)::value;
       const int s = base + J;
       if (GUARD && s >= s1) return;
-      const float x = lrow[4 * (rb + J)];  // zero outside the image (loader)
+      const float x = xa;  // zero outside the image (loader)
+      xa = xb;
+      if (J + 2 < L) xb = lrow[4 * (rb + J + 2)];
       const float yv = cascade<J, L, D, PASSES, BORDER>(
           hd, hlast, x, a, b, BORDER ? gtab + (s - gpos0) + GOFF : gtab);
       if (KIND == 1 || (GUARD && s >= s0 + 2 * HALO)) {
