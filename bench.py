@@ -450,8 +450,14 @@ def run_strips(args, rank, world, dev):
     total = float(t.item())
     px = 3 * size * size
     plans = sf.plans_host()
+    # r >= 9 runs the split sweep: K1 (3) + plan + 2 kernels per term + K4
+    r_sp, _ = P.extended_box_params(p["sigma_s"], 3)
+    if r_sp >= 9:
+        per_step = sum(4 + 2 * (pl.N // 2 - pl.M + 1) + 1 for pl in plans)
+    else:
+        per_step = KERNELS_PER_IMAGE * 3
     return dict(value=px * args.steps / (total * 1e-3) / 1e6, ms_per_step=total / args.steps,
-                launches=(KERNELS_PER_IMAGE * 3) * args.steps, clocks=clk.summary(),
+                launches=per_step * args.steps, clocks=clk.summary(),
                 config=dict(workload=p["name"], channels=3, H=size, W=size, sigma_s=p["sigma_s"],
                             sigma_r=p["sigma_r"], epsilon=p["epsilon"],
                             plans=[(pl.T, pl.N, pl.M) for pl in plans],
