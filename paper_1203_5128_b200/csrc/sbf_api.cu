@@ -2,6 +2,8 @@
 #include <stdarg.h>
 #include <string.h>
 
+#include <type_traits>
+
 #include <vector>
 
 #include "sbf_common.cuh"
@@ -145,22 +147,26 @@ __global__ void epilogue_kernel(const ACC* __restrict__ nd, int groups, int64_t 
                                 const FT* __restrict__ f, int64_t ld, int64_t out_lo,
                                 const double* __restrict__ stats, OT* __restrict__ out,
                                 unsigned long long* __restrict__ fallback) {
+  // one row segment per CTA (no 64-bit index division); fp32 arithmetic when
+  // both the accumulator and the output are fp32
+  using MT = std::conditional_t<std::is_same<ACC, float>::value && std::is_same<OT, float>::value,
+                                float, double>;
   const int used = min(groups, plan->K_eval);
-  const double center = stats[3];
-  const int64_t n = rows * W;
+  const MT center = (MT)stats[3];  // fp32-rounded by K1: exact in either type
   unsigned long long bad_count = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double num = 0.0, den = 0.0;
-    for (int g = 0; g < used; ++g) {
-      num += (double)nd[2 * (g * gstride + i)];
-      den += (double)nd[2 * (g * gstride + i) + 1];
+  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t y = blockIdx.y; y < rows; y += gridDim.y) {
+    if (x < W) {
+      const int64_t i = y * W + x;
+      MT num = 0, den = 0;
+      for (int g = 0; g < used; ++g) {
+        num += (MT)nd[2 * (g * gstride + i)];
+        den += (MT)nd[2 * (g * gstride + i) + 1];
+      }
+      const bool bad = !(den > (MT)0);  // bilateral.py:244 (NaN counts as bad)
+      out[i] = bad ? (OT)f[(out_lo + y) * ld + x] : (OT)(num / den + center);
+      bad_count += bad ? 1 : 0;
     }
-    const int64_t y = i / W, x = i - y * W;
-    const bool bad = !(den > 0.0);  // bilateral.py:244 (NaN counts as bad)
-    const double o = bad ? (double)f[(out_lo + y) * ld + x] : num / den + center;
-    out[i] = (OT)o;
-    bad_count += bad ? 1 : 0;
   }
   for (int o = 16; o; o >>= 1) bad_count += __shfl_xor_sync(0xffffffffu, bad_count, o);
   if ((threadIdx.x & 31) == 0 && bad_count) atomicAdd(fallback, bad_count);
@@ -169,8 +175,8 @@ __global__ void epilogue_kernel(const ACC* __restrict__ nd, int groups, int64_t 
 template <typename ACC>
 static int launch_epilogue(const FilterLaunch& a, const ACC* nd, int groups, int64_t gstride) {
   const int64_t rows = a.out_hi - a.out_lo;
-  const int64_t n = rows * a.W;
-  const unsigned grid = (unsigned)smin<int64_t>((n + 255) / 256, 148 * 8);
+  const dim3 grid((unsigned)((a.W + 255) / 256),
+                  (unsigned)smin<int64_t>(rows, smax<int64_t>(1, 148 * 16 / ((a.W + 255) / 256))));
 #define SBF_EPI(FT, OT)                                                                      \
   epilogue_kernel<ACC, FT, OT><<<grid, 256, 0, a.stream>>>(                                  \
       nd, groups, gstride, a.plan, rows, a.W, static_cast<const FT*>(a.f), a.ld, a.out_lo, \
