@@ -392,8 +392,11 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
             const float2 yb = cascade2<J, L, D, PASSES, BORDER>(
                 st.dl[IMGS / 2 - 1], st.vlast[IMGS / 2 - 1], make_float2(cv, sv), a2, nb2, b2, gt);
             if (!GUARD || t >= 2 * HALO) {
-              float* vp = VB + (t - t0) * VBP + 4 * q;
-              *reinterpret_cast<float4*>(vp) = make_float4(ya.x, ya.y, yb.x, yb.y);
+              // two 8-byte stores straight from the FFMA2 register pairs (one
+              // 16-byte store needed ~7 MOVs per step to build a register quad)
+              float2* vp = reinterpret_cast<float2*>(VB + (t - t0) * VBP + 4 * q);
+              vp[0] = ya;
+              vp[1] = yb;
             }
           } else {
             // one pair per thread: (f v, v), v = cos (pair 0) or sin (pair 1)
