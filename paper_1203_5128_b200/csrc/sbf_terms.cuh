@@ -65,6 +65,9 @@ struct TermParams {
 #ifndef SBF_V_MAIN_VARIANT
 #define SBF_V_MAIN_VARIANT 0  // separate unchecked V block variant for whole blocks (bigger code: slower)
 #endif
+#ifndef SBF_TRIG_AHEAD
+#define SBF_TRIG_AHEAD 0  // phasor of step t+1 computed during step t (r=4: -2%, r=5: +0.5%)
+#endif
 #ifndef SBF_F_EARLY
 #define SBF_F_EARLY 1  // read the next step's sample one step early
 #endif
@@ -322,8 +325,26 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
     for (int j = 0; j < L; ++j) fetch_async(j, j);
     // the sample of step t is read from the ring one step early (step t-1),
     // so its shared-memory latency hides behind a whole step of work
+    // phasor of this pixel for the current term: frac(f nu) by explicit range
+    // reduction (|u| < 2^22), then MUFU sin/cos (IMGS==2: cos or sin per thread)
+    auto phasor = [&](float fcv, float& cv, float& sv) {
+      const float u = fcv * nu;
+      const float tt = u - ((u + 12582912.f) - 12582912.f);
+      if (IMGS == 4) {
+        __sincosf(tt * 6.28318530717958647f, &sv, &cv);
+      } else {
+        cv = __cosf((tt - 0.25f * pair) * 6.28318530717958647f);
+        sv = cv;
+      }
+    };
     cp_async_wait<L - 1>();
     float fnext = fr[0];
+#if SBF_TRIG_AHEAD
+    float fc_ahead = fnext - centerf, ph_c, ph_s;
+    phasor(fc_ahead, ph_c, ph_s);
+    cp_async_wait<L - 2>();
+    fnext = fr[1 % L];
+#endif
 
     for (int t0 = 0; t0 < T_total; t0 += ROWS) {
       const int t1 = min(t0 + ROWS, T_total);
@@ -341,6 +362,16 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
           constexpr int J = decltype(jc)::value;
           const int t = base + J;
           if (KIND >= 1 && (unsigned)(t - t0) >= (unsigned)(t1 - t0)) return;
+#if SBF_TRIG_AHEAD
+          // the phasor of step t was computed during step t-1 (its chain then
+          // overlaps the previous step's recurrences); prepare step t+1 now
+          const float fc = fc_ahead;
+          float cv = ph_c, sv = ph_s;
+          fc_ahead = fnext - centerf;
+          phasor(fc_ahead, ph_c, ph_s);
+          cp_async_wait<(L >= 3 ? L - 3 : 0)>();  // group of step t+2 has landed
+          fnext = fr[(J + 2) % L];
+#else
 #if SBF_F_EARLY
           const float fc = fnext - centerf;
           cp_async_wait<L - 2>();  // group of step t+1 has landed
@@ -349,16 +380,9 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
           cp_async_wait<L - 1>();
           const float fc = fr[J] - centerf;
 #endif
-          // phasor of this pixel for the current term
-          const float u = fc * nu;
-          const float tt = u - ((u + 12582912.f) - 12582912.f);  // frac, |u| < 2^22
           float cv, sv;
-          if (IMGS == 4) {
-            __sincosf(tt * 6.28318530717958647f, &sv, &cv);
-          } else {
-            cv = __cosf((tt - 0.25f * pair) * 6.28318530717958647f);
-            sv = cv;
-          }
+          phasor(fc, cv, sv);
+#endif
           if (BORDER) {  // rows outside the image contribute nothing (zero padding)
             const float m = (grow0 + t >= 0 && grow0 + t < p.img_H) ? 1.f : 0.f;
             cv *= m;
