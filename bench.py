@@ -218,8 +218,10 @@ def run_ours(args, rank, world, dev):
     H, W = img_np.shape
     f = torch.from_numpy(np.ascontiguousarray(img_np)).to(dev)
     dt = _lib.SBF_F64 if f.dtype == torch.float64 else _lib.SBF_F32
-    params = P.FilterParams(sigma_s=p["sigma_s"], sigma_r=p["sigma_r"], epsilon=p["epsilon"],
-                            precision="fp32")
+    # default parameters, as a user calls it (precision "auto": fp32 kernels
+    # with the device-side HDR guard); the device-resident step below passes
+    # SBF_PREC_FP32 explicitly, which runs the same kernels
+    params = P.FilterParams(sigma_s=p["sigma_s"], sigma_r=p["sigma_r"], epsilon=p["epsilon"])
     sp = to_c_spatial(params.resolved_spatial())
     R = params.resolved_radius()
     prec = _lib.PREC_FP32

@@ -68,11 +68,15 @@ extern "C" {
 /* precision modes of the term kernel */
 #define SBF_PREC_FP32 0   /* fp32 phases, sums and accumulators (8-bit-scale images) */
 #define SBF_PREC_HDR 1    /* fp64 running sums and num/den accumulators (16-bit scale) */
+#define SBF_PREC_AUTO 2   /* fp32 kernels, guarded on the device: if max|f - centre| > 4096
+                             the term kernel does nothing and sets SBF_PLAN_NEEDS_HDR
+                             (the caller re-runs with SBF_PREC_HDR); no host sync */
 
 /* plan flags */
 #define SBF_PLAN_N_AMBIGUOUS 1     /* ceil(0.405 x^2) changes within +-2 ulp of x^2 */
 #define SBF_PLAN_EXACT_BIGINT 2    /* exact rule resolved by the multi-limb path */
 #define SBF_PLAN_TERMS_TRUNCATED 4 /* term table capacity exceeded (status set) */
+#define SBF_PLAN_NEEDS_HDR 8       /* SBF_PREC_AUTO found a wide intensity range */
 
 typedef struct sbf_plan {
   double T;        /* dynamic range the plan was built for */

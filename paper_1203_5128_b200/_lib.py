@@ -19,8 +19,8 @@ SBF_OK, SBF_ERR_INVALID, SBF_ERR_UNSUPPORTED, SBF_ERR_CUDA, SBF_ERR_WORKSPACE = 
 SBF_F32, SBF_F64 = 0, 1
 RULES = {"auto": 0, "exact": 1, "chernoff": 2, "none": 3}
 SPATIAL_ITERATED, SPATIAL_BOX = 0, 1
-PREC_FP32, PREC_HDR = 0, 1
-PLAN_N_AMBIGUOUS, PLAN_EXACT_BIGINT, PLAN_TERMS_TRUNCATED = 1, 2, 4
+PREC_FP32, PREC_HDR, PREC_AUTO = 0, 1, 2
+PLAN_N_AMBIGUOUS, PLAN_EXACT_BIGINT, PLAN_TERMS_TRUNCATED, PLAN_NEEDS_HDR = 1, 2, 4, 8
 
 
 class SbfPlan(C.Structure):

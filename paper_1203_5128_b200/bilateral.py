@@ -80,13 +80,15 @@ def _plan_from_struct(p: _lib.SbfPlan) -> KernelPlan:
                       N=int(p.N), M=int(p.M), epsilon=float(p.epsilon))
 
 
-def _precision_code(params, stats_host) -> int:
+def _precision_code(params) -> int:
+    """"auto" runs the fp32 kernels with a device-side range guard
+    (SBF_PREC_AUTO): a wide-range (HDR) image is detected on the GPU and
+    re-run with the fp64 path, so the common case needs no host round trip."""
     if params.precision == "fp32":
         return _lib.PREC_FP32
     if params.precision == "hdr":
         return _lib.PREC_HDR
-    mn, mx, c = stats_host[1], stats_host[2], stats_host[3]
-    return _lib.PREC_HDR if max(abs(mx - c), abs(mn - c)) > HDR_THRESHOLD else _lib.PREC_FP32
+    return _lib.PREC_AUTO
 
 
 def shiftable_bf(img, params: FilterParams) -> ShiftableResult:
@@ -113,9 +115,9 @@ def shiftable_bf(img, params: FilterParams) -> ShiftableResult:
 def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False):
     """K1..K4 on a staged device image; returns (output, KernelPlan, fallbacks).
 
-    With an explicit precision mode the pipeline runs without a host round
-    trip and synchronises once at the end (non-finite input is still
-    rejected, after the fact); "auto" reads the intensity range after K1.
+    The pipeline runs without a host round trip and synchronises once at the
+    end (non-finite input is rejected after the fact); "auto" resolves fp32
+    vs HDR on the device and re-runs the fp64 path only for wide ranges.
     `to_host` copies the result into pinned host memory (cached allocator).
     """
     import torch
@@ -131,13 +133,7 @@ def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False
     use_fixed = params.fixed_T is not None
     # K1: T (or only the statistics when T is fixed)
     stats, _ = local_range(s, 0 if use_fixed else radius)
-    if params.precision == "auto":
-        st = stats.cpu().numpy()
-        if int(st[7:8].view(np.uint64)[0]) != 0:
-            raise InvalidParameterError("image contains non-finite samples")
-        prec = _precision_code(params, st)
-    else:
-        prec = _precision_code(params, None)
+    prec = _precision_code(params)
     stream = _stream_ptr()
     plan_dev = torch.empty(64, dtype=torch.uint8, device=dev)
     terms = torch.empty(TERMS_CAP * 32, dtype=torch.uint8, device=dev)
@@ -175,19 +171,27 @@ def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False
     if int(tail[72:].view(np.uint64)[7]) != 0:
         raise InvalidParameterError("image contains non-finite samples")
     _lib.check(plan_c.status, "plan")
+
+    def rerun():
+        fb.zero_()
+        _lib.check(lib.sbf_filter(s.tensor.data_ptr(), s.dtype, H, W, W, 0, H, 0, H, sp,
+                                  plan_dev.data_ptr(), terms.data_ptr(), stats.data_ptr(),
+                                  prec, out_dev.data_ptr(), out_dtype, fb.data_ptr(),
+                                  ws.data_ptr(), ws.numel(), stream), "filter")
+        if to_host:
+            out.copy_(out_dev)
+        return (_lib.SbfPlan.from_buffer_copy(plan_dev.cpu().numpy().tobytes()),
+                int(fb.item()))
+
+    if plan_c.flags & _lib.PLAN_NEEDS_HDR:
+        # the device guard found |f - centre| > 4096: fp64 path
+        prec = _lib.PREC_HDR
+        plan_c, fallbacks = rerun()
     if plan_c.flags & _lib.PLAN_N_AMBIGUOUS:
         # ceil(0.405 q^2) straddles an integer within 2 ulp of q^2: the host twin
         # (libm pow, bit-equal to CPython) decides, and the filter is re-run
         ph = select_plan(plan_c.T, params.sigma_r, params.epsilon, truncation=params.truncation)
         if (ph.N, ph.M) != (plan_c.N, plan_c.M):
             plan_on_device(forced=(ph.N, ph.M))
-            fb.zero_()
-            _lib.check(lib.sbf_filter(s.tensor.data_ptr(), s.dtype, H, W, W, 0, H, 0, H, sp,
-                                      plan_dev.data_ptr(), terms.data_ptr(), stats.data_ptr(),
-                                      prec, out_dev.data_ptr(), out_dtype, fb.data_ptr(),
-                                      ws.data_ptr(), ws.numel(), stream), "filter")
-            if to_host:
-                out.copy_(out_dev)
-            plan_c = _lib.SbfPlan.from_buffer_copy(plan_dev.cpu().numpy().tobytes())
-            fallbacks = int(fb.item())
+            plan_c, fallbacks = rerun()
     return out, _plan_from_struct(plan_c), fallbacks

@@ -114,6 +114,9 @@ static bool spatial_coeffs(const sbf_spatial& sp, int* r, int* passes, double* a
 // partial accumulators (+ an fp32 centred copy of float64 inputs for K3)
 size_t filter_ws(int64_t H, int64_t W, int64_t rows_out, int dtype, const sbf_spatial* sp,
                  int precision) {
+  if (precision == SBF_PREC_AUTO)  // either path may run
+    return smax(filter_ws(H, W, rows_out, dtype, sp, SBF_PREC_FP32),
+                filter_ws(H, W, rows_out, dtype, sp, SBF_PREC_HDR));
   if (find_split(*sp, precision)) {
     // split sweep: accumulator + column-smoothed images of one term
     size_t bytes = align_up((size_t)(rows_out * W) * 8) + align_up((size_t)(rows_out * W) * 16);
@@ -195,6 +198,8 @@ static thread_local int g_stage_mask = 3;
 // fp64 evaluation choice: 0 = always the term sweeps, 1 = cost model, 2 = dual
 // whenever exact (M = 0)
 static thread_local int g_dual_mode = 1;
+// set while an SBF_PREC_AUTO call runs the guarded fp32 term kernel
+static thread_local int g_hdr_guard = 0;
 
 // fp32 input view for the term kernels: fp64 inputs get a centred fp32 copy
 static const float* f32_view(const FilterLaunch& a, void* scratch, int64_t* ld, int* centred) {
@@ -275,8 +280,27 @@ int launch_filter(const FilterLaunch& a) {
               "bad output row range");
   SBF_REQUIRE(a.row0 >= 0 && a.row0 + a.H <= a.img_H, SBF_ERR_INVALID, "bad global row range");
   SBF_REQUIRE(spatial_coeffs(a.sp, &r, &passes, &alpha), SBF_ERR_INVALID, "bad spatial mode");
-  SBF_REQUIRE(a.precision == SBF_PREC_FP32 || a.precision == SBF_PREC_HDR, SBF_ERR_INVALID,
-              "bad precision mode");
+  SBF_REQUIRE(a.precision == SBF_PREC_FP32 || a.precision == SBF_PREC_HDR ||
+                  a.precision == SBF_PREC_AUTO,
+              SBF_ERR_INVALID, "bad precision mode");
+  if (a.precision == SBF_PREC_AUTO) {
+    // the K3 path checks the range on the device; every other path reads
+    // the plan on the host anyway, so it resolves the mode there
+    FilterLaunch b = a;
+    b.precision = SBF_PREC_FP32;
+    const TermsEntry* e3 = find_entry(b.sp, SBF_PREC_FP32);
+    if (!e3 || find_split(b.sp, SBF_PREC_FP32)) {
+      double st[8];
+      SBF_CHECK_CUDA(cudaMemcpyAsync(st, a.stats, sizeof(st), cudaMemcpyDeviceToHost, a.stream));
+      SBF_CHECK_CUDA(cudaStreamSynchronize(a.stream));
+      if (fmax(st[2] - st[3], st[3] - st[1]) > 4096.0) b.precision = SBF_PREC_HDR;
+      return launch_filter(b);
+    }
+    g_hdr_guard = 1;
+    const int rc = launch_filter(b);
+    g_hdr_guard = 0;
+    return rc;
+  }
   // the buffer must hold every row within the spatial support of the outputs
   const int64_t sup = (int64_t)passes * (r + 1);
   SBF_REQUIRE((a.out_lo - sup >= 0 || a.row0 == 0) &&
@@ -348,6 +372,7 @@ int launch_filter(const FilterLaunch& a) {
   p.nd = a.ws;
   p.nd_group_stride = rows_out * a.W;
   p.counter = reinterpret_cast<int*>(static_cast<char*>(a.ws) + nd_bytes - 256);
+  p.hdr_guard = g_hdr_guard;
   if (g_stage_mask & 1) {
     SBF_CHECK_CUDA(cudaMemsetAsync(a.ws, 0, nd_bytes, a.stream));
   }

@@ -60,7 +60,15 @@ struct TermParams {
   const double* stats;
   void* nd;
   int64_t nd_group_stride;  // (num, den) pairs per group
+  int hdr_guard;            // SBF_PREC_AUTO: bail out (flag the plan) on wide ranges
 };
+
+// SBF_PREC_AUTO guard: the fp32 kernels are accurate to the north-star
+// tolerance only while |f - centre| stays within the 8-bit-scale regime
+__device__ __forceinline__ bool needs_hdr(const double* stats) {
+  const double c = stats[3];
+  return fmax(stats[2] - c, c - stats[1]) > 4096.0;
+}
 
 #ifndef SBF_V_MAIN_VARIANT
 #define SBF_V_MAIN_VARIANT 0  // separate unchecked V block variant for whole blocks (bigger code: slower)
@@ -239,6 +247,11 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
 
   const sbf_plan* plan = p.plan;
   if (plan->status != SBF_OK) return;
+  if (p.hdr_guard && needs_hdr(p.stats)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      atomicOr(const_cast<int*>(&plan->flags), SBF_PLAN_NEEDS_HDR);
+    return;
+  }
   const int K_eval = plan->K_eval;
   const int units = p.nstrips * p.nbands;
   const int total = K_eval * units;

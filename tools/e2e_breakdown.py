@@ -15,7 +15,7 @@ from paper_1203_5128_b200.workloads import config_image  # noqa: E402
 
 img = config_image(2)
 pinned = torch.from_numpy(np.ascontiguousarray(img)).pin_memory()
-params = P.FilterParams(sigma_s=5, sigma_r=10, epsilon=0.01, precision="fp32")
+params = P.FilterParams(sigma_s=5, sigma_r=10, epsilon=0.01)
 for _ in range(5):
     P.shiftable_bf(pinned, params)
 torch.cuda.synchronize()
