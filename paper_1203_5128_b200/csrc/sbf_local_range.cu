@@ -2,11 +2,11 @@
 //
 // Separable windowed maximum over the clamped (2R+1)^2 window, followed by
 // T = max(M - f) evaluated in float64 exactly like the reference
-// (`float(np.max(max_filter_2d(f, R) - f))`).  Both line passes use the van
-// Herk / Gil-Werman partition scheme on shared-memory tiles: replicate
-// padding (equivalent to clamping the window), per-partition prefix and
-// suffix maxima, one combining max per output.  Max is exact, so M is
-// bit-identical to the reference whatever the partition alignment.
+// (`float(np.max(max_filter_2d(f, R) - f))`).  Both line passes stage a
+// replicate-padded tile in shared memory (padding == clamping the window)
+// and build power-of-two span maxima by doubling (log2(2R+1) fully parallel
+// steps); each output is the max of two overlapping spans.  Max is exact, so
+// M is bit-identical to the reference whatever the evaluation order.
 //
 // HBM-bound: f is read twice (row pass, column pass) and the row maxima
 // once (written + read); T, min f and max f are reduced on chip and folded
@@ -39,29 +39,29 @@ __global__ void __launch_bounds__(256) rowmax_kernel(const T* __restrict__ f, in
   const int plen = nblk * win;
   T* suf = q + plen;
   const T* row = f + y * ld;
-  for (int k = threadIdx.x; k < plen; k += blockDim.x) {
+  // loads batched 4 deep per thread (independent, so they overlap in flight)
+#pragma unroll 4
+  for (int k = threadIdx.x; k < len; k += blockDim.x) {
     int64_t x = x0 - R + k;
     x = x < 0 ? 0 : (x >= W ? W - 1 : x);
-    q[k] = row[x];
+    q[k] = __ldg(row + x);
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
-    const int s = b * win;
-    T acc = q[s + win - 1];
-    suf[s + win - 1] = acc;
-    for (int k = win - 2; k >= 0; --k) {
-      acc = vmax(acc, q[s + k]);
-      suf[s + k] = acc;
-    }
-    acc = q[s];
-    for (int k = 1; k < win; ++k) {  // prefix max in place
-      acc = vmax(acc, q[s + k]);
-      q[s + k] = acc;
-    }
+  // doubling: a[i] = max over [i, i + span) (every element in parallel,
+  // log2(win) steps), then each output is the max of two overlapping spans
+  T* a = q;
+  T* b = suf;
+  int span = 1;
+  while (2 * span <= win) {
+    for (int i = threadIdx.x; i <= len - 2 * span; i += blockDim.x) b[i] = vmax(a[i], a[i + span]);
+    __syncthreads();
+    T* t = a;
+    a = b;
+    b = t;
+    span *= 2;
   }
-  __syncthreads();
   T* orow = out + y * W + x0;
-  for (int j = threadIdx.x; j < nout; j += blockDim.x) orow[j] = vmax(suf[j], q[j + 2 * R]);
+  for (int j = threadIdx.x; j < nout; j += blockDim.x) orow[j] = vmax(a[j], a[j + win - span]);
 }
 
 __device__ __forceinline__ void finalize_stats(double* stats) {
@@ -118,33 +118,35 @@ __global__ void __launch_bounds__(kColTile* kColThreadsY) colmax_kernel(
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int64_t x = (int64_t)blockIdx.x * kColTile + tx;
   const bool xok = x < W;
-  for (int k = ty; k < plen; k += kColThreadsY) {
-    int64_t y = y0 - R + k;
-    y = y < 0 ? 0 : (y >= H ? H - 1 : y);
-    q[k * P + tx] = xok ? rowmax[y * W + x] : T(0);
-  }
-  __syncthreads();
-  for (int b = ty; b < nblk; b += kColThreadsY) {
-    const int s = b * win;
-    T acc = q[(s + win - 1) * P + tx];
-    suf[(s + win - 1) * P + tx] = acc;
-    for (int k = win - 2; k >= 0; --k) {
-      acc = vmax(acc, q[(s + k) * P + tx]);
-      suf[(s + k) * P + tx] = acc;
-    }
-    acc = q[s * P + tx];
-    for (int k = 1; k < win; ++k) {
-      acc = vmax(acc, q[(s + k) * P + tx]);
-      q[(s + k) * P + tx] = acc;
+  {
+    const T* colp = rowmax + (xok ? x : 0);
+#pragma unroll 8
+    for (int k = ty; k < len; k += kColThreadsY) {
+      int64_t y = y0 - R + k;
+      y = y < 0 ? 0 : (y >= H ? H - 1 : y);
+      q[k * P + tx] = xok ? __ldg(colp + y * W) : T(0);
     }
   }
   __syncthreads();
+  // doubling along the column (see rowmax_kernel)
+  T* a = q;
+  T* bb = suf;
+  int span = 1;
+  while (2 * span <= win) {
+    for (int i = ty; i <= len - 2 * span; i += kColThreadsY)
+      bb[i * P + tx] = vmax(a[i * P + tx], a[(i + span) * P + tx]);
+    __syncthreads();
+    T* t = a;
+    a = bb;
+    bb = t;
+    span *= 2;
+  }
   double tmax = 0.0, fmn = INFINITY, fmx = -INFINITY;
   unsigned long long bad = 0;
   if (xok) {
     for (int j = ty; j < nrows; j += kColThreadsY) {
       const int64_t y = y0 + j;
-      const T m = vmax(suf[j * P + tx], q[(j + 2 * R) * P + tx]);
+      const T m = vmax(a[j * P + tx], a[(j + win - span) * P + tx]);
       if (M_out) M_out[y * W + x] = m;
       if (y >= t_lo && y < t_hi) {
         const double fv = (double)f[y * ld + x];
