@@ -92,3 +92,43 @@ def test_plan_reflects_computed_t_and_fixed_t():
     assert res.plan == P.select_plan(P.compute_T(img, 2), 30, 0.01)
     res = _bf(img[:16, :16], sigma_s=2, sigma_r=30, spatial=P.Box(2), fixed_T=255.0)
     assert res.plan.T == 255.0
+
+
+def _random_case(seed):
+    rng = np.random.default_rng(seed)
+    h, w = int(rng.integers(1, 260)), int(rng.integers(1, 260))
+    kind = rng.choice(["u8", "f32", "f64", "u16"])
+    hi = 65535.0 if kind == "u16" else 255.0
+    img = rng.uniform(0, hi, (h, w))
+    if rng.random() < 0.5:  # piecewise-constant regions + noise, like the configs
+        img = np.where(np.add.outer(np.arange(h), np.arange(w)) % 37 < 18, 0.2 * hi, 0.7 * hi)
+        img = img + rng.normal(0, hi / 40, (h, w))
+    if kind == "u8":
+        img = np.clip(np.round(img), 0, 255).astype(np.uint8)
+    elif kind == "u16":
+        img = np.clip(np.round(img), 0, 65535).astype(np.uint16)
+    elif kind == "f32":
+        img = img.astype(np.float32)
+    sigma_s = float(rng.choice([0.7, 1.5, 3.0, 5.0, 6.0, 9.7, 11.6]))
+    sigma_r = float(rng.choice([8.0, 20.0, 45.0, 90.0])) * (257.0 if kind == "u16" else 1.0)
+    eps = float(rng.choice([0.0, 0.01, 0.05]))
+    box = rng.random() < 0.25
+    fixed = None if rng.random() < 0.8 else float(hi)
+    return img, sigma_s, sigma_r, eps, box, fixed
+
+
+@pytest.mark.parametrize("seed", range(64))
+def test_random_cases_vs_c_oracle(seed):
+    """Seeded random shapes / dtypes / parameters (incl. 16-bit HDR, box mode,
+    fixed T, the split sweep at r >= 9) against the C oracle."""
+    from oracle import coracle as CO
+    CO.build()
+    img, ss, sr, eps, box, fixed = _random_case(seed)
+    spatial = P.Box(max(1, int(round(ss)))) if box else None
+    osp = ("box", max(1, int(round(ss)))) if box else None
+    res = P.shiftable_bf(img, P.FilterParams(sigma_s=ss, sigma_r=sr, epsilon=eps, spatial=spatial,
+                                             fixed_T=fixed))
+    ref = CO.shiftable_bf(np.asarray(img, dtype=np.float64), ss, sr, eps, spatial=osp, fixed_T=fixed)
+    assert (res.plan.T, res.plan.N, res.plan.M) == (ref["T"], ref["N"], ref["M"])
+    d = np.abs(res.image - ref["image"])
+    assert float(d.max()) <= TOL and float(np.sqrt(np.mean(d * d))) <= 1e-3, (img.dtype, img.shape, ss, sr, eps, box)
