@@ -253,7 +253,19 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
     return;
   }
   const int K_eval = plan->K_eval;
-  const int units = p.nstrips * p.nbands;
+  // band height from the device plan: the largest band (smem is sized for
+  // p.band) that still gives >= 2 items per CTA; small images / few terms
+  // get shorter bands instead of leaving most SMs idle (halo cost <= 1.5x)
+  int bandh = p.band;
+  {
+    const int rows_out = p.out_hi - p.out_lo;
+    const int per_band = max(1, p.nstrips * K_eval);
+    const int nb_min = (2 * (int)gridDim.x + per_band - 1) / per_band;
+    const int b = (rows_out + nb_min - 1) / nb_min;
+    bandh = max(min(b, p.band), min(4 * HALO, p.band));
+  }
+  const int nbands = (p.out_hi - p.out_lo + bandh - 1) / bandh;
+  const int units = p.nstrips * nbands;
   const int total = K_eval * units;
   const int tid = threadIdx.x;
   const float centerf = p.centred ? 0.f : (float)p.stats[3];
@@ -275,15 +287,16 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
     const int si = u - band * p.nstrips;
     const int strip = p.nstrips < 2 ? si : (si == 0 ? 0 : (si == 1 ? p.nstrips - 1 : si - 1));
 
-  const int y0 = p.out_lo + band * p.band;
-  const int y1 = min(p.out_hi, y0 + p.band);
+  const int y0 = p.out_lo + band * bandh;
+  const int y1 = min(p.out_hi, y0 + bandh);
   const int Bn = y1 - y0;
   const int T_total = Bn + 2 * HALO;
   const int xs = strip * WC - HALO;  // image column of haloed index 0
 
   // ---- border tables: index = stream/haloed position + GOFF ----
   const int64_t grow0 = p.row0 + (int64_t)(y0 - HALO);  // global row of stream position 0
-  for (int k = tid; k < gv_len; k += THREADS) gv[k] = gfactor(grow0 + (k - GOFF), p.img_H, p.r, p.alpha);
+  for (int k = tid; k < bandh + 2 * HALO + GOFF; k += THREADS)
+    gv[k] = gfactor(grow0 + (k - GOFF), p.img_H, p.r, p.alpha);
   for (int k = tid; k < HALO_W + GOFF; k += THREADS)
     gh[k] = gfactor((int64_t)xs + (k - GOFF), p.W, p.r, p.alpha);
   // stream positions whose rows have factor 1 (conservative: D from the edges)
