@@ -59,8 +59,12 @@ struct SplitCfg {
 };
 
 // ============================ SV: column sweep ============================
+#ifndef SBF_SV_MINB
+#define SBF_SV_MINB 1  // SV CTAs per SM the register allocation must allow
+#endif
+
 template <int R, int PASSES>
-__global__ void __launch_bounds__(SplitCfg<R, PASSES>::SV_THREADS)
+__global__ void __launch_bounds__(SplitCfg<R, PASSES>::SV_THREADS, SBF_SV_MINB)
     sv_kernel(const SplitParams p) {
   using C = SplitCfg<R, PASSES>;
   constexpr int D = C::D, L = C::L, HALO = C::HALO, IMGS = C::IMGS, GOFF = C::GOFF;
