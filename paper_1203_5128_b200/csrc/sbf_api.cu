@@ -633,6 +633,20 @@ int sbf_shiftable_bf_host(const double* f_host, int64_t H, int64_t W, const sbf_
     rc = sbf_shiftable_bf(f_dev, SBF_F64, H, W, sp, R, fixed_T, sigma_r, epsilon, rule,
                           log_2_over_eps, precision, o_dev, SBF_F64, plan_dev, stats_dev, fb_dev,
                           cap, ws, ws_bytes, st);
+  if (rc == SBF_OK && precision == SBF_PREC_AUTO) {
+    // the guarded fp32 kernel flags wide-range images: re-run on the fp64 path
+    sbf_plan pl;
+    if (cudaMemcpyAsync(&pl, plan_dev, sizeof(pl), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+      rc = SBF_ERR_CUDA;
+    } else if (pl.flags & SBF_PLAN_NEEDS_HDR) {
+      if (cudaMemsetAsync(fb_dev, 0, sizeof(unsigned long long), st) != cudaSuccess) rc = SBF_ERR_CUDA;
+      if (rc == SBF_OK)
+        rc = sbf_shiftable_bf(f_dev, SBF_F64, H, W, sp, R, fixed_T, sigma_r, epsilon, rule,
+                              log_2_over_eps, SBF_PREC_HDR, o_dev, SBF_F64, plan_dev, stats_dev,
+                              fb_dev, cap, ws, ws_bytes, st);
+    }
+  }
   if (rc == SBF_OK) {
     if (cudaMemcpyAsync(out_host, o_dev, img, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaMemcpyAsync(plan_out, plan_dev, sizeof(sbf_plan), cudaMemcpyDeviceToHost, st) !=

@@ -127,3 +127,30 @@ def test_cli_direct_method_and_bench_with_direct(tmp_path, capsys):
                      "--repeats", "1", "--with-direct", "--csv", log]) == 0
     rows = list(csv.reader(open(log)))[1:]
     assert len(rows) == 2 and all(float(r[9]) < 5.0 for r in rows)
+
+
+@pytest.mark.gpu
+def test_standalone_c_caller_of_the_abi(tmp_path):
+    """tests/c_abi/sbf_example.c links libsbf.so directly (no Python in the
+    call path) and must reproduce the oracle."""
+    import os
+    import subprocess
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "sbf_example")
+    lib_dir = os.path.join(repo, "paper_1203_5128_b200")
+    subprocess.run(["gcc", "-O2", "-o", exe, os.path.join(repo, "tests", "c_abi", "sbf_example.c"),
+                    "-I", os.path.join(repo, "include"), "-L", lib_dir, "-lsbf",
+                    "-L/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{lib_dir}",
+                    "-Wl,-rpath,/usr/local/cuda/lib64", "-lm"], check=True)
+    for kind in ("u8", "hdr"):
+        rng = np.random.default_rng(9)
+        img = rng.uniform(0, 65535 if kind == "hdr" else 255, (70, 90))
+        src, dst = str(tmp_path / "in.f8"), str(tmp_path / "out.f8")
+        img.astype("<f8").tofile(src)
+        sr = 2000.0 if kind == "hdr" else 25.0
+        res = subprocess.run([exe, src, dst, "70", "90", "3.0", str(sr), "0.01"], check=True,
+                             capture_output=True, text=True)
+        ref = O.shiftable_bf(img, 3.0, sr, 0.01)
+        assert f"N={ref['N']} M={ref['M']}" in res.stdout
+        got = np.fromfile(dst, dtype="<f8").reshape(img.shape)
+        assert np.abs(got - ref["image"]).max() <= 1e-2
