@@ -64,6 +64,7 @@ extern "C" {
 /* spatial modes (spatial.py:24-42) */
 #define SBF_SPATIAL_ITERATED 0
 #define SBF_SPATIAL_BOX 1
+#define SBF_SPATIAL_FIR 2        /* sampled Gaussian taps, radius r (sbf_smooth / direct only) */
 
 /* precision modes of the term kernel */
 #define SBF_PREC_FP32 0   /* fp32 phases, sums and accumulators (8-bit-scale images) */
@@ -218,6 +219,13 @@ int sbf_direct_bf(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, in
                   const double* taps_host, double sigma_r, int precision, void* out,
                   int out_dtype, void* stream);
 
+/* Same, with the truncated raised-cosine expansion as the range kernel
+ * (bilateral.py:101-103 expansion_range): K(s) = sum_k scale[k] cos(freq[k] s)
+ * over K <= 1024 folded terms (host arrays), float64. */
+int sbf_direct_bf_expansion(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int R,
+                            const double* taps_host, const double* scale, const double* freq,
+                            int K, void* out, int out_dtype, void* stream);
+
 /* ---- coarse non-local means (reference nlm.py:78-137) ----
  * One item = one folded multi-index of the per-component expansions and one
  * cos/sin choice for components j >= 1 (bit j of `mask`); component 0
@@ -238,6 +246,22 @@ int sbf_nlm_filter(const void* f, int dtype, int64_t H, int64_t W, int64_t ld,
                    const sbf_spatial* sp, int p, const int32_t* offsets,
                    const sbf_nlm_item* items, int n_items, const double* stats, void* out,
                    int out_dtype, unsigned long long* fallback, void* stream);
+
+/* Brute-force coarse NLM (nlm.py:140-183 direct_nlm): window weights taps
+ * (NULL: uniform), p patch offsets (first = origin, replicate padding) and per
+ * component range kernel kinds[j] = 0 Gaussian(sigmas[j]) or 1 truncated
+ * expansion (nterms[j] folded terms, consecutive in scale/freq); float64. */
+int sbf_direct_nlm(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int R,
+                   const double* taps_host, int p, const int32_t* offsets, const int32_t* kinds,
+                   const double* sigmas, const int32_t* nterms, const double* scale,
+                   const double* freq, void* out, int out_dtype, void* stream);
+
+/* ---- standalone spatial smoothers (spatial.py:65-182) ----
+ * box_filter (BOX, r), iterated_box_gaussian (ITERATED: passes, r, alpha),
+ * fir_gaussian (FIR: sigma_s, r); float64 arithmetic, exact clamped
+ * renormalisation.  out is H x W (ld = W).  Allocates stream-ordered. */
+int sbf_smooth(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, const sbf_spatial* sp,
+               void* out, int out_dtype, void* stream);
 
 /* ---- introspection / benchmarking hooks ---- */
 /* fp64 (HDR / generic) evaluation, this thread: 0 = always the K term sweeps,

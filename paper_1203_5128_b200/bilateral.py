@@ -195,3 +195,23 @@ def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False
             plan_on_device(forced=(ph.N, ph.M))
             plan_c, fallbacks = rerun()
     return out, _plan_from_struct(plan_c), fallbacks
+
+
+def shiftable_bf_poly(img, params: FilterParams) -> ShiftableResult:
+    """bilateral.py:167-202 — the polynomial range family is outside the CUDA path."""
+    raise InvalidParameterError("the polynomial family is not supported by the CUDA path")
+
+
+# backend registry of the reference (_core/__init__.py:12-71): one CUDA backend
+def available_backends():
+    return ["cuda"]
+
+
+def backend_name() -> str:
+    return "cuda"
+
+
+def use_backend(name: str) -> str:
+    if name != "cuda":
+        raise ValueError(f"unknown backend {name!r}; choices: ['cuda']")
+    return "cuda"

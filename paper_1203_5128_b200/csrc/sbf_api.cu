@@ -108,7 +108,8 @@ static bool spatial_coeffs(const sbf_spatial& sp, int* r, int* passes, double* a
     *passes = sp.passes;
     *alpha = sp.alpha;
   }
-  return *r >= 0 && *passes >= 1 && *alpha >= 0.0 && *alpha < 1.0;
+  return (sp.mode == SBF_SPATIAL_BOX || sp.mode == SBF_SPATIAL_ITERATED) && *r >= 0 &&
+         *passes >= 1 && *alpha >= 0.0 && *alpha < 1.0;
 }
 
 // partial accumulators (+ an fp32 centred copy of float64 inputs for K3)

@@ -98,6 +98,49 @@ __global__ void __launch_bounds__(256) direct_kernel(const FT* __restrict__ f, O
   if (two) out[(y0 + 1) * p.W + x] = (OT)(d1 > 0.f ? n1 / d1 : c1);
 }
 
+// truncated raised-cosine expansion as the range kernel (reference
+// bilateral.py:101-103 expansion_range): K(s) = sum_k scale_k cos(w_k s)
+// over the folded terms, float64 (the exact-shiftability oracle)
+constexpr int kDirectMaxTerms = 1024;
+struct DirectTerms {
+  int K;
+  double scale[kDirectMaxTerms];
+  double freq[kDirectMaxTerms];
+};
+
+template <typename FT, typename OT>
+__global__ void __launch_bounds__(256) direct_terms_kernel(const FT* __restrict__ f,
+                                                           OT* __restrict__ out,
+                                                           const __grid_constant__ DirectParams p,
+                                                           const DirectTerms* __restrict__ tt) {
+  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t y = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= p.W || y >= p.H) return;
+  const int R = p.R;
+  const double c = (double)f[y * p.ld + x];
+  const int dx_lo = (int)smax<int64_t>(-R, -x), dx_hi = (int)smin<int64_t>(R, p.W - 1 - x);
+  const int dy_lo = (int)smax<int64_t>(-R, -y), dy_hi = (int)smin<int64_t>(R, p.H - 1 - y);
+  const int K = tt->K;
+  double num = 0.0, den = 0.0;
+  for (int dy = dy_lo; dy <= dy_hi; ++dy) {
+    const FT* row = f + (y + dy) * p.ld + x;
+    const double wy = p.tap[dy + R];
+    if (wy == 0.0) continue;
+    for (int dx = dx_lo; dx <= dx_hi; ++dx) {
+      const double wsp = wy * p.tap[dx + R];
+      if (wsp == 0.0) continue;
+      const double v = (double)row[dx];
+      const double d = v - c;
+      double k = 0.0;
+      for (int t = 0; t < K; ++t) k += tt->scale[t] * cos(tt->freq[t] * d);
+      const double w = wsp * k;
+      num += w * v;
+      den += w;
+    }
+  }
+  out[y * p.W + x] = (OT)(den > 0.0 ? num / den : c);
+}
+
 template <typename FT, typename OT>
 int launch_direct(const void* f, void* out, const DirectParams& p, int f64math, cudaStream_t st) {
   dim3 block(32, 8);
@@ -151,4 +194,52 @@ extern "C" int sbf_direct_bf(const void* f, int dtype, int64_t H, int64_t W, int
                                 : launch_direct<float, double>(f, out, p, f64math, st);
   return out_dtype == SBF_F32 ? launch_direct<double, float>(f, out, p, f64math, st)
                               : launch_direct<double, double>(f, out, p, f64math, st);
+}
+
+extern "C" int sbf_direct_bf_expansion(const void* f, int dtype, int64_t H, int64_t W, int64_t ld,
+                                       int R, const double* taps, const double* scale,
+                                       const double* freq, int K, void* out, int out_dtype,
+                                       void* stream) {
+  using namespace sbf;
+  SBF_REQUIRE(f && out && scale && freq, SBF_ERR_INVALID, "null pointer");
+  SBF_REQUIRE(dtype == SBF_F32 || dtype == SBF_F64, SBF_ERR_INVALID, "bad dtype");
+  SBF_REQUIRE(out_dtype == SBF_F32 || out_dtype == SBF_F64, SBF_ERR_INVALID, "bad out dtype");
+  SBF_REQUIRE(H >= 1 && W >= 1 && ld >= W, SBF_ERR_INVALID, "bad image shape");
+  SBF_REQUIRE(R >= 0 && R <= kDirectMaxR, SBF_ERR_UNSUPPORTED, "direct_bf radius %d outside [0, %d]",
+              R, kDirectMaxR);
+  SBF_REQUIRE(K >= 1 && K <= kDirectMaxTerms, SBF_ERR_UNSUPPORTED, "expansion of %d terms", K);
+  DirectParams p;
+  memset(&p, 0, sizeof(p));
+  p.H = H;
+  p.W = W;
+  p.ld = ld;
+  p.R = R;
+  for (int k = 0; k <= 2 * R; ++k) {
+    const double t = taps ? taps[k] : 1.0;
+    SBF_REQUIRE(t >= 0.0 && t == t, SBF_ERR_INVALID, "spatial taps must be non-negative");
+    p.tap[k] = t;
+  }
+  DirectTerms ht;
+  ht.K = K;
+  for (int k = 0; k < K; ++k) {
+    ht.scale[k] = scale[k];
+    ht.freq[k] = freq[k];
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DirectTerms* dt = nullptr;
+  SBF_CHECK_CUDA(cudaMallocAsync(&dt, sizeof(DirectTerms), st));
+  SBF_CHECK_CUDA(cudaMemcpyAsync(dt, &ht, sizeof(DirectTerms), cudaMemcpyHostToDevice, st));
+  const dim3 block(32, 8), grid((unsigned)((W + 31) / 32), (unsigned)((H + 7) / 8));
+#define SBF_DT(FT, OT)                                                                        \
+  direct_terms_kernel<FT, OT><<<grid, block, 0, st>>>(static_cast<const FT*>(f),              \
+                                                      static_cast<OT*>(out), p, dt)
+  if (dtype == SBF_F32 && out_dtype == SBF_F32) SBF_DT(float, float);
+  else if (dtype == SBF_F32) SBF_DT(float, double);
+  else if (out_dtype == SBF_F32) SBF_DT(double, float);
+  else SBF_DT(double, double);
+#undef SBF_DT
+  SBF_CHECK_LAUNCH();
+  // the pageable source was staged by cudaMemcpyAsync before it returned
+  SBF_CHECK_CUDA(cudaFreeAsync(dt, st));
+  return SBF_OK;
 }

@@ -201,22 +201,23 @@ int PlaneSmoother::init(const sbf_spatial& sp, int64_t H_, int64_t W_, int64_t r
   return SBF_OK;
 }
 
-int PlaneSmoother::run(double* planes, double* tmp, cudaStream_t st) const {
+int PlaneSmoother::run(double* planes, double* tmp, cudaStream_t st, int nplanes) const {
   const int bs = 256;
   const dim3 tb(32, 8);
   if (fused) {
     // input: tmp [pl][W][H] (rows as columns); output planes [pl][H][W]
-    const dim3 tgridT((unsigned)((H + 31) / 32), (unsigned)((W + 31) / 32), 4);
+    const dim3 tgridT((unsigned)((H + 31) / 32), (unsigned)((W + 31) / 32), (unsigned)nplanes);
     const int64_t seg = 256;
-    fe->launch(tmp, planes, 4, W, H, seg, gx, 0, W, ca, cb, st);                // row passes
-    transpose_planes<<<tgridT, tb, 0, st>>>(planes, tmp, W, H);                 // -> [pl][H][W]
-    fe->launch(tmp, planes, 4, H, W, seg, gy, row0, img_H, ca, cb, st);         // column passes
+    fe->launch(tmp, planes, nplanes, W, H, seg, gx, 0, W, ca, cb, st);                // row passes
+    transpose_planes<<<tgridT, tb, 0, st>>>(planes, tmp, W, H);                       // -> [pl][H][W]
+    fe->launch(tmp, planes, nplanes, H, W, seg, gy, row0, img_H, ca, cb, st);         // column passes
   } else {
     // input and output: planes [pl][H][W]
     for (int ps = 0; ps < passes; ++ps) {
-      gen_rows<<<(unsigned)((4 * H + bs - 1) / bs), bs, 0, st>>>(planes, tmp, 4 * H, W, r, alpha);
-      gen_cols<<<(unsigned)((4 * W + bs - 1) / bs), bs, 0, st>>>(tmp, planes, 4, H, W, row0, img_H,
-                                                                 r, alpha);
+      gen_rows<<<(unsigned)((nplanes * H + bs - 1) / bs), bs, 0, st>>>(planes, tmp, nplanes * H, W,
+                                                                       r, alpha);
+      gen_cols<<<(unsigned)((nplanes * W + bs - 1) / bs), bs, 0, st>>>(tmp, planes, nplanes, H, W,
+                                                                       row0, img_H, r, alpha);
     }
   }
   SBF_CHECK_LAUNCH();

@@ -22,7 +22,7 @@ struct PlaneSmoother {
   double* gy = nullptr;
   int init(const sbf_spatial& sp, int64_t H, int64_t W, int64_t row0, int64_t img_H,
            cudaStream_t st);
-  int run(double* planes, double* tmp, cudaStream_t st) const;
+  int run(double* planes, double* tmp, cudaStream_t st, int nplanes = 4) const;
   void release(cudaStream_t st);
 };
 

@@ -210,3 +210,128 @@ extern "C" int sbf_nlm_filter(const void* f, int dtype, int64_t H, int64_t W, in
   SBF_CHECK_CUDA(cudaFreeAsync(nd, st));
   return SBF_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Brute-force coarse NLM (reference nlm.py:140-183 direct_nlm): for every
+// in-bounds window offset d, w = w_s(d) prod_j K_j(f_j(x+d) - f_j(x)) with
+// f_j the replicate-padded copy of f shifted by u_j; out = sum w f / sum w.
+// K_j is a Gaussian of width sigma_j or a truncated cosine expansion
+// (expansion_range_for), float64.  The test oracle of the shiftable NLM.
+// ---------------------------------------------------------------------------
+namespace sbf {
+namespace {
+
+constexpr int kNlmMaxR = 128, kNlmMaxTerms = 256;
+struct DirectNlmParams {
+  int64_t H, W, ld;
+  int R, p;
+  int dy[3], dx[3];
+  int kind[3];  // 0 Gaussian, 1 expansion
+  double inv[3];  // 1 / (2 sigma^2)
+  int K[3];
+  double scale[3][kNlmMaxTerms], freq[3][kNlmMaxTerms];
+  double tap[2 * kNlmMaxR + 1];
+};
+
+template <typename FT, typename OT>
+__global__ void __launch_bounds__(256) direct_nlm_kernel(const FT* __restrict__ f,
+                                                         OT* __restrict__ out,
+                                                         const __grid_constant__ DirectNlmParams q) {
+  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t y = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= q.W || y >= q.H) return;
+  auto at = [&](int64_t yy, int64_t xx) -> double {
+    yy = yy < 0 ? 0 : (yy >= q.H ? q.H - 1 : yy);
+    xx = xx < 0 ? 0 : (xx >= q.W ? q.W - 1 : xx);
+    return (double)f[yy * q.ld + xx];
+  };
+  double cj[3];
+  for (int j = 0; j < q.p; ++j) cj[j] = at(y + q.dy[j], x + q.dx[j]);
+  const int R = q.R;
+  const int dy_lo = (int)smax<int64_t>(-R, -y), dy_hi = (int)smin<int64_t>(R, q.H - 1 - y);
+  const int dx_lo = (int)smax<int64_t>(-R, -x), dx_hi = (int)smin<int64_t>(R, q.W - 1 - x);
+  double num = 0.0, den = 0.0;
+  for (int dy = dy_lo; dy <= dy_hi; ++dy) {
+    for (int dx = dx_lo; dx <= dx_hi; ++dx) {
+      double w = q.tap[dy + R] * q.tap[dx + R];
+      if (w == 0.0) continue;
+      for (int j = 0; j < q.p; ++j) {
+        const double s = at(y + dy + q.dy[j], x + dx + q.dx[j]) - cj[j];
+        if (q.kind[j] == 0) {
+          w *= exp(-(s * s) * q.inv[j]);
+        } else {
+          double k = 0.0;
+          for (int t = 0; t < q.K[j]; ++t) k += q.scale[j][t] * cos(q.freq[j][t] * s);
+          w *= k;
+        }
+      }
+      const double v = (double)f[(y + dy) * q.ld + x + dx];
+      num += w * v;
+      den += w;
+    }
+  }
+  out[y * q.W + x] = (OT)(den > 0.0 ? num / den : (double)f[y * q.ld + x]);
+}
+
+}  // namespace
+}  // namespace sbf
+
+extern "C" int sbf_direct_nlm(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int R,
+                              const double* taps, int p, const int32_t* offsets,
+                              const int32_t* kinds, const double* sigmas, const int32_t* nterms,
+                              const double* scale, const double* freq, void* out, int out_dtype,
+                              void* stream) {
+  using namespace sbf;
+  SBF_REQUIRE(f && out && offsets && kinds, SBF_ERR_INVALID, "null pointer");
+  SBF_REQUIRE(dtype == SBF_F32 || dtype == SBF_F64, SBF_ERR_INVALID, "bad dtype");
+  SBF_REQUIRE(out_dtype == SBF_F32 || out_dtype == SBF_F64, SBF_ERR_INVALID, "bad out dtype");
+  SBF_REQUIRE(H >= 1 && W >= 1 && ld >= W, SBF_ERR_INVALID, "bad image shape");
+  SBF_REQUIRE(p >= 1 && p <= 3, SBF_ERR_INVALID, "patch must have 1 to 3 offsets");
+  SBF_REQUIRE(R >= 0 && R <= kNlmMaxR, SBF_ERR_UNSUPPORTED, "radius %d outside [0, %d]", R, kNlmMaxR);
+  DirectNlmParams* q = new DirectNlmParams();
+  q->H = H;
+  q->W = W;
+  q->ld = ld;
+  q->R = R;
+  q->p = p;
+  int off = 0;
+  for (int j = 0; j < p; ++j) {
+    q->dy[j] = offsets[2 * j];
+    q->dx[j] = offsets[2 * j + 1];
+    q->kind[j] = kinds[j];
+    if (kinds[j] == 0) {
+      if (!(sigmas && sigmas[j] > 0.0)) {
+        delete q;
+        set_error("Gaussian range kernels need sigma > 0");
+        return SBF_ERR_INVALID;
+      }
+      q->inv[j] = 1.0 / (2.0 * sigmas[j] * sigmas[j]);
+    } else {
+      const int K = nterms ? nterms[j] : 0;
+      if (!(K >= 1 && K <= kNlmMaxTerms && scale && freq)) {
+        delete q;
+        set_error("expansion range kernels need 1..%d terms", kNlmMaxTerms);
+        return SBF_ERR_UNSUPPORTED;
+      }
+      q->K[j] = K;
+      for (int t = 0; t < K; ++t) {
+        q->scale[j][t] = scale[off + t];
+        q->freq[j][t] = freq[off + t];
+      }
+      off += K;
+    }
+  }
+  for (int k = 0; k <= 2 * R; ++k) q->tap[k] = taps ? taps[k] : 1.0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const dim3 block(32, 8), grid((unsigned)((W + 31) / 32), (unsigned)((H + 7) / 8));
+#define SBF_DN(FT, OT) \
+  direct_nlm_kernel<FT, OT><<<grid, block, 0, st>>>(static_cast<const FT*>(f), static_cast<OT*>(out), *q)
+  if (dtype == SBF_F32 && out_dtype == SBF_F32) SBF_DN(float, float);
+  else if (dtype == SBF_F32) SBF_DN(float, double);
+  else if (out_dtype == SBF_F32) SBF_DN(double, float);
+  else SBF_DN(double, double);
+#undef SBF_DN
+  delete q;
+  SBF_CHECK_LAUNCH();
+  return SBF_OK;
+}

@@ -35,6 +35,36 @@ class GaussianRange:
         return np.exp(-(s * s) * (1.0 / (2.0 * self.sigma_r * self.sigma_r)))
 
 
+@dataclass(frozen=True)
+class ExpansionRange:
+    """The truncated cosine expansion itself as a range kernel (bilateral.py:101-103)."""
+
+    expansion: object
+
+    def __call__(self, s):
+        from .kernels import eval_truncated_kernel
+        return eval_truncated_kernel(self.expansion, s)
+
+
+def expansion_range(expansion) -> ExpansionRange:
+    """Range kernel evaluating a truncated raised-cosine expansion (bilateral.py:101-103);
+    direct_bf with it is the exact-shiftability oracle, run on the GPU in fp64."""
+    return ExpansionRange(expansion)
+
+
+def polynomial_range(plan):
+    """(1 - s^2 / (2 N sigma_r^2))^N (bilateral.py:106-114): host-side kernel
+    function only — the polynomial family is not part of the CUDA path, so
+    direct_bf rejects it."""
+    a = 2.0 * plan.N * plan.sigma_r ** 2
+
+    def kernel(s):
+        s = np.asarray(s, dtype=np.float64)
+        return (1.0 - (s * s) / a) ** plan.N
+
+    return kernel
+
+
 def gaussian_range(sigma_r) -> GaussianRange:
     """Vectorised Gaussian range kernel of width sigma_r (bilateral.py:88-99)."""
     if sigma_r <= 0:
@@ -79,9 +109,9 @@ def direct_bf(img, spatial, range_kernel, radius=None):
     """
     import torch
 
-    if not isinstance(range_kernel, GaussianRange):
+    if not isinstance(range_kernel, (GaussianRange, ExpansionRange)):
         raise InvalidParameterError(
-            "only gaussian_range() kernels run on the GPU direct path")
+            "only gaussian_range() / expansion_range() kernels run on the GPU direct path")
     if radius is None:
         if isinstance(spatial, (Box, FirGaussian)):
             radius = spatial.radius
@@ -103,6 +133,19 @@ def direct_bf(img, spatial, range_kernel, radius=None):
     out = torch.empty((s.H, s.W), dtype=torch.float64 if out_f64 else torch.float32,
                       device=s.tensor.device)
     lib = _lib.load()
+    if isinstance(range_kernel, ExpansionRange):
+        e = range_kernel.expansion
+        keep = 2 * np.asarray(e.indices) <= e.plan.N  # fold +-w (cos is even)
+        w = np.asarray(e.weights)[keep]
+        n = np.asarray(e.indices)[keep]
+        scale = np.ascontiguousarray(np.where(2 * n == e.plan.N, w, 2.0 * w), dtype=np.float64)
+        freq = np.ascontiguousarray(np.asarray(e.frequencies)[keep], dtype=np.float64)
+        _lib.check(lib.sbf_direct_bf_expansion(
+            s.tensor.data_ptr(), s.dtype, s.H, s.W, s.W, radius,
+            None if taps is None else taps.ctypes.data, scale.ctypes.data, freq.ctypes.data,
+            len(scale), out.data_ptr(), _lib.SBF_F64 if out_f64 else _lib.SBF_F32, _stream_ptr()),
+            "direct_bf")
+        return out.cpu().numpy() if numpy_in else (out.cpu() if s.host else out)
     _lib.check(lib.sbf_direct_bf(s.tensor.data_ptr(), s.dtype, s.H, s.W, s.W, radius,
                                  None if taps is None else taps.ctypes.data,
                                  float(range_kernel.sigma_r),

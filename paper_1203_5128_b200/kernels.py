@@ -201,3 +201,8 @@ def eval_gaussian(s, sigma_r):
 
 def polynomial_unsupported(*_a, **_k):
     raise UnsupportedOrderError("the polynomial family is not supported by the CUDA path")
+
+
+def polynomial_shift_coefficients(plan, tau):
+    """kernels.py:272-276 — polynomial family, outside the CUDA path."""
+    polynomial_unsupported()

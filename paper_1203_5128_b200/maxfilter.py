@@ -78,3 +78,10 @@ def compute_T(img, radius) -> float:
     if radius == 0:
         return 0.0
     return float(st[0])
+
+
+def brute_force_T(img, radius) -> float:
+    """max over windows of |f(y) - f(x)| (maxfilter.py:64-): by the paper's
+    Proposition 1 this equals max(M - f), which K1 computes exactly, so the
+    brute-force scan is not repeated on the GPU."""
+    return compute_T(img, radius)

@@ -162,3 +162,65 @@ def coarse_nlm_shiftable(img, patch: PatchSpec, spatial: SpatialMode, radius: in
         warnings.warn(f"{fallbacks} pixel(s) had a non-positive normalizer; input values kept",
                       RuntimeWarning, stacklevel=2)
     return NlmResult(out.cpu().numpy() if numpy_in else (out.cpu() if s.host else out), plans, fallbacks)
+
+
+def expansion_range_for(plan: KernelPlan):
+    """Truncated-expansion range kernel of one NLM component (nlm.py:186-189)."""
+    from .direct import expansion_range
+    return expansion_range(raised_cosine_expansion(plan))
+
+
+def direct_nlm(img, patch: PatchSpec, spatial: SpatialMode, radius: int,
+               range_kernels="gaussian"):
+    """Literal windowed coarse NLM (nlm.py:140-183), the shiftable NLM's test
+    oracle, on the GPU (`sbf_direct_nlm`, float64).  `range_kernels` is
+    "gaussian" or one gaussian_range / expansion_range kernel per component."""
+    import torch
+
+    from .direct import ExpansionRange, GaussianRange, _taps
+
+    radius = int(radius)
+    if range_kernels == "gaussian":
+        from .direct import gaussian_range
+        kernels = [gaussian_range(sg) for sg in patch.sigmas]
+    else:
+        kernels = list(range_kernels)
+        if len(kernels) != patch.size:
+            raise InvalidParameterError("need one range kernel per patch offset")
+    taps = _taps(spatial, radius)
+    kinds, sigmas, nterms, scales, freqs = [], [], [], [], []
+    for k in kernels:
+        if isinstance(k, GaussianRange):
+            kinds.append(0)
+            sigmas.append(k.sigma_r)
+            nterms.append(0)
+        elif isinstance(k, ExpansionRange):
+            e = k.expansion
+            keep = 2 * np.asarray(e.indices) <= e.plan.N
+            w = np.asarray(e.weights)[keep]
+            n = np.asarray(e.indices)[keep]
+            kinds.append(1)
+            sigmas.append(0.0)
+            nterms.append(int(keep.sum()))
+            scales.extend(np.where(2 * n == e.plan.N, w, 2.0 * w).tolist())
+            freqs.extend(np.asarray(e.frequencies)[keep].tolist())
+        else:
+            raise InvalidParameterError(
+                "only gaussian_range() / expansion_range() kernels run on the GPU direct path")
+    s = stage(img)
+    stats, _ = local_range(s, 0)
+    if _nonfinite(stats.cpu().numpy()):
+        raise InvalidParameterError("image contains non-finite samples")
+    numpy_in = s.host and not s.torch_in
+    out_f64 = numpy_in or s.dtype == _lib.SBF_F64
+    out = torch.empty((s.H, s.W), dtype=torch.float64 if out_f64 else torch.float32,
+                      device=s.tensor.device)
+    i32 = lambda v: (C.c_int32 * max(1, len(v)))(*v)
+    f64 = lambda v: (C.c_double * max(1, len(v)))(*v)
+    _lib.check(_lib.load().sbf_direct_nlm(
+        s.tensor.data_ptr(), s.dtype, s.H, s.W, s.W, radius,
+        None if taps is None else taps.ctypes.data, patch.size,
+        i32([v for off in patch.offsets for v in off]), i32(kinds), f64(sigmas), i32(nterms),
+        f64(scales), f64(freqs), out.data_ptr(), _lib.SBF_F64 if out_f64 else _lib.SBF_F32,
+        _stream_ptr()), "direct_nlm")
+    return out.cpu().numpy() if numpy_in else (out.cpu() if s.host else out)

@@ -232,6 +232,36 @@ def nlm_cases():
     np.savez_compressed(os.path.join(HERE, "nlm.npz"), **out)
 
 
+def direct_nlm_cases():
+    """direct_nlm (nlm.py:140-183) with Gaussian and expansion range kernels."""
+    from shiftbf import nlm as rn
+    rng = np.random.default_rng(20260813)
+    cases = [
+        # (h, w, offsets, sigmas, spatial, radius, kernels)
+        (20, 23, [(0, 0), (0, 1)], [40.0, 30.0], ("box", 2), 2, "gaussian"),
+        (18, 16, [(0, 0), (1, 0), (0, -1)], [50.0, 50.0, 60.0], ("fir", 1.5, 3), 3, "gaussian"),
+        (16, 21, [(0, 0), (1, 1)], [40.0, 40.0], ("box", 3), 3, "expansion"),
+    ]
+    out = {}
+    for k, (h, w, offs, sgs, sp, rad, kern) in enumerate(cases):
+        img = rng.uniform(0, 120, (h, w))
+        mode = rs.Box(sp[1]) if sp[0] == "box" else rs.FirGaussian(sp[1], sp[2])
+        patch = rn.PatchSpec(tuple(offs), tuple(sgs))
+        if kern == "gaussian":
+            ref = rn.direct_nlm(img, patch, mode, rad)
+        else:
+            T = rm.compute_T(img, rad + patch.max_offset_norm)
+            plans = [rk.select_plan(T, sg, 0.05) for sg in sgs]
+            ref = rn.direct_nlm(img, patch, mode, rad, [rn.expansion_range_for(pl) for pl in plans])
+        out[f"img_{k}"] = img
+        out[f"offs_{k}"] = np.array(offs, dtype=np.int64)
+        out[f"par_{k}"] = np.array(sgs + [0 if sp[0] == "box" else 1, sp[1],
+                                          sp[1] if sp[0] == "box" else sp[2], rad,
+                                          0 if kern == "gaussian" else 1])
+        out[f"out_{k}"] = ref
+    np.savez_compressed(os.path.join(HERE, "direct_nlm.npz"), **out)
+
+
 def big_plans():
     rows = []
     specs = [(2, 0, 5.0, 10.0), (3, 0, 8.0, 800.0)] + [(4, i, 6.0, 20.0) for i in range(64)] \
@@ -255,6 +285,7 @@ if __name__ == "__main__":
     if a.direct:
         direct_cases()
         nlm_cases()
+        direct_nlm_cases()
     elif not a.big:
         plans()
         maxfilters()
@@ -263,6 +294,7 @@ if __name__ == "__main__":
         config1()
         direct_cases()
         nlm_cases()
+        direct_nlm_cases()
     if a.big:
         big_plans()
     print("done")
