@@ -79,6 +79,12 @@ __device__ __forceinline__ bool needs_hdr(const double* stats) {
 #ifndef SBF_F_EARLY
 #define SBF_F_EARLY 1  // read the next step's sample one step early
 #endif
+#ifndef SBF_TAIL_ROWS
+#define SBF_TAIL_ROWS 128  // band height of the tail terms (0: no tail)
+#endif
+#ifndef SBF_TAIL_WAVES
+#define SBF_TAIL_WAVES 2   // tail items ~ this many per CTA
+#endif
 #ifndef SBF_H_FIXED_SEQ
 #define SBF_H_FIXED_SEQ 1  // interior strips: warm-up / main-loop / tail H blocks, no dispatch
 #endif
@@ -264,9 +270,21 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
     const int b = (rows_out + nb_min - 1) / nb_min;
     bandh = max(min(b, p.band), min(4 * HALO, p.band));
   }
-  const int nbands = (p.out_hi - p.out_lo + bandh - 1) / bandh;
+  const int rows_all = p.out_hi - p.out_lo;
+  const int nbands = (rows_all + bandh - 1) / bandh;
   const int units = p.nstrips * nbands;
-  const int total = K_eval * units;
+  // tail: the last Ks terms run in short bands, so the queue ends with small
+  // items and CTAs finish together (with one band size for every term, SMs
+  // idled ~18% of the kernel waiting for the last long items)
+  int Ks = 0, bands_s = 1, units_s = 0;
+  if (SBF_TAIL_ROWS > 0 && bandh > SBF_TAIL_ROWS) {
+    bands_s = (rows_all + SBF_TAIL_ROWS - 1) / SBF_TAIL_ROWS;
+    units_s = p.nstrips * bands_s;
+    Ks = min(K_eval / 4, (SBF_TAIL_WAVES * (int)gridDim.x + units_s - 1) / units_s);
+  }
+  const int bandh_s = (rows_all + bands_s - 1) / bands_s;
+  const int items_big = (K_eval - Ks) * units;
+  const int total = items_big + Ks * units_s;
   const int tid = threadIdx.x;
   const float centerf = p.centred ? 0.f : (float)p.stats[3];
   const float a = p.a, b = p.b;
@@ -281,21 +299,25 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
     __syncthreads();
     const int item = s_item;
     if (item >= total) break;
-    const int kk = item / units;
-    const int u = item - kk * units;
+    const bool tail = item >= items_big;
+    const int i2 = tail ? item - items_big : item;
+    const int un = tail ? units_s : units;
+    const int kk = (tail ? K_eval - Ks : 0) + i2 / un;
+    const int u = i2 - (i2 / un) * un;
     const int band = u / p.nstrips;
     const int si = u - band * p.nstrips;
     const int strip = p.nstrips < 2 ? si : (si == 0 ? 0 : (si == 1 ? p.nstrips - 1 : si - 1));
+    const int bh = tail ? bandh_s : bandh;
 
-  const int y0 = p.out_lo + band * bandh;
-  const int y1 = min(p.out_hi, y0 + bandh);
+  const int y0 = p.out_lo + band * bh;
+  const int y1 = min(p.out_hi, y0 + bh);
   const int Bn = y1 - y0;
   const int T_total = Bn + 2 * HALO;
   const int xs = strip * WC - HALO;  // image column of haloed index 0
 
   // ---- border tables: index = stream/haloed position + GOFF ----
   const int64_t grow0 = p.row0 + (int64_t)(y0 - HALO);  // global row of stream position 0
-  for (int k = tid; k < bandh + 2 * HALO + GOFF; k += THREADS)
+  for (int k = tid; k < bh + 2 * HALO + GOFF; k += THREADS)
     gv[k] = gfactor(grow0 + (k - GOFF), p.img_H, p.r, p.alpha);
   for (int k = tid; k < HALO_W + GOFF; k += THREADS)
     gh[k] = gfactor((int64_t)xs + (k - GOFF), p.W, p.r, p.alpha);
