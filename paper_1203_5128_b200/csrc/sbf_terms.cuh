@@ -85,6 +85,9 @@ __device__ __forceinline__ bool needs_hdr(const double* stats) {
 #ifndef SBF_TAIL_WAVES
 #define SBF_TAIL_WAVES 2   // tail items ~ this many per CTA
 #endif
+#ifndef SBF_TAIL2
+#define SBF_TAIL2 0  // last tail terms in half-height bands again (measured: slower)
+#endif
 #ifndef SBF_H_FIXED_SEQ
 #define SBF_H_FIXED_SEQ 1  // interior strips: warm-up / main-loop / tail H blocks, no dispatch
 #endif
@@ -283,8 +286,17 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
     Ks = min(K_eval / 4, (SBF_TAIL_WAVES * (int)gridDim.x + units_s - 1) / units_s);
   }
   const int bandh_s = (rows_all + bands_s - 1) / bands_s;
+  // the very last terms of the tail in bands half as tall again
+  int Ks2 = 0, bands_s2 = 1, units_s2 = 0;
+  if (SBF_TAIL2 && Ks >= 2 && bandh_s >= 2 * 4 * HALO) {
+    bands_s2 = 2 * bands_s;
+    units_s2 = p.nstrips * bands_s2;
+    Ks2 = min(Ks / 2, ((int)gridDim.x + units_s2 - 1) / units_s2);
+  }
+  const int bandh_s2 = (rows_all + bands_s2 - 1) / bands_s2;
   const int items_big = (K_eval - Ks) * units;
-  const int total = items_big + Ks * units_s;
+  const int items_mid = (Ks - Ks2) * units_s;
+  const int total = items_big + items_mid + Ks2 * units_s2;
   const int tid = threadIdx.x;
   const float centerf = p.centred ? 0.f : (float)p.stats[3];
   const float a = p.a, b = p.b;
@@ -299,15 +311,15 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
     __syncthreads();
     const int item = s_item;
     if (item >= total) break;
-    const bool tail = item >= items_big;
-    const int i2 = tail ? item - items_big : item;
-    const int un = tail ? units_s : units;
-    const int kk = (tail ? K_eval - Ks : 0) + i2 / un;
+    const int seg = item < items_big ? 0 : (item < items_big + items_mid ? 1 : 2);
+    const int i2 = seg == 0 ? item : (seg == 1 ? item - items_big : item - items_big - items_mid);
+    const int un = seg == 0 ? units : (seg == 1 ? units_s : units_s2);
+    const int kk = (seg == 0 ? 0 : (seg == 1 ? K_eval - Ks : K_eval - Ks2)) + i2 / un;
     const int u = i2 - (i2 / un) * un;
     const int band = u / p.nstrips;
     const int si = u - band * p.nstrips;
     const int strip = p.nstrips < 2 ? si : (si == 0 ? 0 : (si == 1 ? p.nstrips - 1 : si - 1));
-    const int bh = tail ? bandh_s : bandh;
+    const int bh = seg == 0 ? bandh : (seg == 1 ? bandh_s : bandh_s2);
 
   const int y0 = p.out_lo + band * bh;
   const int y1 = min(p.out_hi, y0 + bh);
