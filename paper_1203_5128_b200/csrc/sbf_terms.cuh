@@ -83,7 +83,10 @@ __device__ __forceinline__ bool needs_hdr(const double* stats) {
 #define SBF_TAIL_ROWS 128  // band height of the tail terms (0: no tail)
 #endif
 #ifndef SBF_TAIL_WAVES
-#define SBF_TAIL_WAVES 2   // tail items ~ this many per CTA
+#define SBF_TAIL_WAVES 3   // tail items ~ this many per CTA (capped at K/SBF_TAIL_FRAC terms)
+#endif
+#ifndef SBF_TAIL_FRAC
+#define SBF_TAIL_FRAC 4   // at most K/4 terms in the tail
 #endif
 #ifndef SBF_TAIL2
 #define SBF_TAIL2 0  // last tail terms in half-height bands again (measured: slower)
@@ -283,7 +286,7 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
   if (SBF_TAIL_ROWS > 0 && bandh > SBF_TAIL_ROWS) {
     bands_s = (rows_all + SBF_TAIL_ROWS - 1) / SBF_TAIL_ROWS;
     units_s = p.nstrips * bands_s;
-    Ks = min(K_eval / 4, (SBF_TAIL_WAVES * (int)gridDim.x + units_s - 1) / units_s);
+    Ks = min(K_eval / SBF_TAIL_FRAC, (SBF_TAIL_WAVES * (int)gridDim.x + units_s - 1) / units_s);
   }
   const int bandh_s = (rows_all + bands_s - 1) / bands_s;
   // the very last terms of the tail in bands half as tall again
