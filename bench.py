@@ -411,8 +411,24 @@ def run_batch(args, rank, world, dev):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     total = float(t.item())
     px = n_img * H * W
+    # algorithmic FP32 ops of the whole batch (132 per pixel per
+    # evaluated folded term); K per image from the host twin of the plan
+    ks = []
+    for f in imgs:
+        pl = P.select_plan(P.compute_T(f, R), p["sigma_r"], p["epsilon"])
+        ks.append(pl.N // 2 - pl.M + 1)
+    kt = torch.tensor([float(sum(ks))], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(kt)
+    ops = OPS_PER_PX_TERM * H * W * float(kt.item())
+    achieved = ops * args.steps / (total * 1e-3) / 1e12
+    peak = 148 * 128 * 1.965e9 / 1e12
     return dict(value=px * args.steps / (total * 1e-3) / 1e6, ms_per_step=total / args.steps,
                 launches=KERNELS_PER_IMAGE * len(mine) * args.steps, clocks=clk.summary(),
+                roofline=dict(bound="fp32", achieved=achieved, peak=peak * world, unit="TFLOP/s",
+                              frac=achieved / (peak * world), traffic=None,
+                              kernel="whole step (K1..K4 over the batch, all ranks)",
+                              ops_basis=f"{OPS_PER_PX_TERM} ops/px/term x {H}x{W} px x sum K = {int(kt.item())}"),
                 config=dict(workload=p["name"], images=n_img, H=H, W=W, sigma_s=p["sigma_s"],
                             sigma_r=p["sigma_r"], epsilon=p["epsilon"],
                             parallelism=f"image batch sharded over {world} rank(s), no collective",
@@ -463,8 +479,15 @@ def run_strips(args, rank, world, dev):
         per_step = sum(4 + 2 * (pl.N // 2 - pl.M + 1) + 1 for pl in plans)
     else:
         per_step = KERNELS_PER_IMAGE * 3
+    ops = OPS_PER_PX_TERM * size * size * sum(pl.N // 2 - pl.M + 1 for pl in plans)
+    achieved = ops * args.steps / (total * 1e-3) / 1e12
+    peak = 148 * 128 * 1.965e9 / 1e12 * world
     return dict(value=px * args.steps / (total * 1e-3) / 1e6, ms_per_step=total / args.steps,
                 launches=per_step * args.steps, clocks=clk.summary(),
+                roofline=dict(bound="fp32", achieved=achieved, peak=peak, unit="TFLOP/s",
+                              frac=achieved / peak, traffic=None,
+                              kernel="whole step (K1, plan, split sweep / K3, K4; 3 channels, all ranks)",
+                              ops_basis=f"{OPS_PER_PX_TERM} ops/px/term x {size}^2 px x sum K over channels"),
                 config=dict(workload=p["name"], channels=3, H=size, W=size, sigma_s=p["sigma_s"],
                             sigma_r=p["sigma_r"], epsilon=p["epsilon"],
                             plans=[(pl.T, pl.N, pl.M) for pl in plans],
@@ -533,7 +556,8 @@ def main():
                         warmup=args.warmup, ms_per_step=r["ms_per_step"], higher_is_better=True,
                         scaling="strong", vs_baseline=None,
                         dtype="f32", data="synthetic (SURVEY.md Appendix A generator, seeded)",
-                        config=r["config"], gpu_launches=r["launches"], clocks=r["clocks"])
+                        config=r["config"], roofline=r.get("roofline"),
+                        gpu_launches=r["launches"], clocks=r["clocks"])
             print(json.dumps(line))
         return
     r = run_ours(args, rank, world, dev)
