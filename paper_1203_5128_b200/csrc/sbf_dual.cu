@@ -122,33 +122,58 @@ __global__ void kernel_table(const sbf_plan* __restrict__ plan, int64_t smax,
     lut[s] = pow_n(cos(g * (double)s), N);
 }
 
+// One CTA per 32 x 8 output tile; the (8 + 2S) x (32 + 2S) input tile and the
+// tile's column / row weights are staged in shared memory, so each tap is one
+// shared-memory read of f, one weight read (broadcast-free layout [dx][col])
+// and one table gather.
 template <typename FT, typename OT>
 __global__ void __launch_bounds__(256) dual_lut_kernel(
     const FT* __restrict__ f, int64_t H, int64_t W, int64_t ld, int64_t out_lo, int64_t out_hi,
     int S, const double* __restrict__ Wr, const double* __restrict__ Wc,
     const double* __restrict__ lut, OT* __restrict__ out, unsigned long long* __restrict__ fallback) {
-  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t yo = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
-  const int64_t y = out_lo + yo;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int T = 2 * S + 1;
+  const int IW = 32 + 2 * S, IH = 8 + 2 * S;
+  double* wcs = reinterpret_cast<double*>(smem_raw);  // [T][32]
+  double* wrs = wcs + T * 32;                           // [8][T]
+  FT* fin = reinterpret_cast<FT*>(wrs + 8 * T);         // [IH][IW]
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  const int64_t x0 = (int64_t)blockIdx.x * 32, yo0 = (int64_t)blockIdx.y * 8;
+  const int64_t y0 = out_lo + yo0;
+  for (int k = tid; k < T * 32; k += 256) {
+    const int d = k / 32, c = k - d * 32;
+    wcs[k] = x0 + c < W ? Wc[(x0 + c) * T + d] : 0.0;
+  }
+  for (int k = tid; k < 8 * T; k += 256) {
+    const int r = k / T, d = k - r * T;
+    wrs[k] = y0 + r < out_hi ? Wr[(yo0 + r) * T + d] : 0.0;
+  }
+  for (int k = tid; k < IH * IW; k += 256) {
+    const int iy = k / IW, ix = k - iy * IW;
+    int64_t gy = y0 - S + iy, gx = x0 - S + ix;
+    // outside the buffer: weight 0 there (the tables hold 0 outside the image)
+    gy = gy < 0 ? 0 : (gy >= H ? H - 1 : gy);
+    gx = gx < 0 ? 0 : (gx >= W ? W - 1 : gx);
+    fin[k] = f[gy * ld + gx];
+  }
+  __syncthreads();
+  const int64_t x = x0 + tx, y = y0 + ty;
   bool bad = false;
   if (x < W && y < out_hi) {
-    const int T = 2 * S + 1;
-    const FT fx = f[y * ld + x];
-    const double* wr = Wr + yo * T;
-    const double* wc = Wc + x * T;
+    const FT fx = fin[(ty + S) * IW + tx + S];
     const int dy_lo = (int)smax<int64_t>(-S, -y), dy_hi = (int)smin<int64_t>(S, H - 1 - y);
     const int dx_lo = (int)smax<int64_t>(-S, -x), dx_hi = (int)smin<int64_t>(S, W - 1 - x);
     double num = 0.0, den = 0.0;
     for (int dy = dy_lo; dy <= dy_hi; ++dy) {
-      const double a = wr[dy + S];
+      const double a = wrs[ty * T + dy + S];
       if (a == 0.0) continue;
-      const FT* frow = f + (y + dy) * ld + x;
+      const FT* frow = fin + (ty + S + dy) * IW + tx + S;
       double rn = 0.0, rd = 0.0;
 #pragma unroll 4
       for (int dx = dx_lo; dx <= dx_hi; ++dx) {
         const FT v = frow[dx];
         const int sd = (int)(v - fx);  // exact: integer samples below 2^24
-        const double w = wc[dx + S] * __ldg(lut + (sd < 0 ? -sd : sd));
+        const double w = wcs[(dx + S) * 32 + tx] * __ldg(lut + (sd < 0 ? -sd : sd));
         rn = fma(w, (double)v, rn);
         rd += w;
       }
@@ -156,7 +181,7 @@ __global__ void __launch_bounds__(256) dual_lut_kernel(
       den = fma(a, rd, den);
     }
     bad = !(den > 0.0);  // bilateral.py:244
-    out[yo * W + x] = (OT)(bad ? (double)fx : num / den);
+    out[(y - out_lo) * W + x] = (OT)(bad ? (double)fx : num / den);
   }
   const unsigned m = __ballot_sync(0xffffffffu, bad);
   if ((threadIdx.x & 31) == 0 && m) atomicAdd(fallback, (unsigned long long)__popc(m));
@@ -275,9 +300,15 @@ int launch_dual_direct(const FilterLaunch& a, const sbf_plan& plan) {
     kernel_table<<<(unsigned)smin<int64_t>((smax_v + 256) / 256, 148 * 8), 256, 0, st>>>(
         a.plan, smax_v, lut);
 #define SBF_DUAL_LUT(FT, OT)                                                                     \
-  dual_lut_kernel<FT, OT><<<grid, tb, 0, st>>>(static_cast<const FT*>(a.f), a.H, a.W, a.ld,      \
+  do {                                                                                           \
+    const size_t smem = sizeof(double) * (size_t)(2 * S + 1) * 40 +                              \
+                        sizeof(FT) * (size_t)(8 + 2 * S) * (32 + 2 * S);                         \
+    SBF_CHECK_CUDA(cudaFuncSetAttribute(dual_lut_kernel<FT, OT>,                                 \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));\
+    dual_lut_kernel<FT, OT><<<grid, tb, smem, st>>>(static_cast<const FT*>(a.f), a.H, a.W, a.ld, \
                                                a.out_lo, a.out_hi, S, Wr, Wc, lut,               \
-                                               static_cast<OT*>(a.out), a.fallback)
+                                               static_cast<OT*>(a.out), a.fallback); \
+  } while (0)
     if (a.dtype == SBF_F32 && a.out_dtype == SBF_F32) SBF_DUAL_LUT(float, float);
     else if (a.dtype == SBF_F32) SBF_DUAL_LUT(float, double);
     else if (a.out_dtype == SBF_F32) SBF_DUAL_LUT(double, float);
