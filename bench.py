@@ -368,13 +368,22 @@ def run_batch(args, rank, world, dev):
     lib = _lib.load()
     p = _cfg_params(args.config)
     n_img = args.images
-    parts = shard_images([1.0] * n_img, world)      # equal pixels; K differs by <= 2 of 12
-    mine = parts[rank]
-    imgs = [torch.from_numpy(np.ascontiguousarray(config_image(4, i))).to(dev) for i in mine]
-    H, W = imgs[0].shape
     params = P.FilterParams(sigma_s=p["sigma_s"], sigma_r=p["sigma_r"], epsilon=p["epsilon"])
     sp = to_c_spatial(params.resolved_spatial())
     R = params.resolved_radius()
+    # balance ranks by px * K.  Every rank plans every image
+    # (K1 + host plan twin, outside the timed region) so the LPT sharding is
+    # identical on all ranks without communication.
+    ks_all = []
+    for i in range(n_img):
+        g = torch.from_numpy(np.ascontiguousarray(config_image(4, i))).to(dev)
+        pl = P.select_plan(P.compute_T(g, R), p["sigma_r"], p["epsilon"])
+        ks_all.append(pl.N // 2 - pl.M + 1)
+        del g
+    parts = shard_images([float(k) for k in ks_all], world)
+    mine = parts[rank]
+    imgs = [torch.from_numpy(np.ascontiguousarray(config_image(4, i))).to(dev) for i in mine]
+    H, W = imgs[0].shape
     cap = 1 << 16
     ws = torch.empty(lib.sbf_shiftable_bf_workspace(H, W, _lib.SBF_F32, sp, _lib.PREC_FP32, cap),
                      dtype=torch.uint8, device=dev)
@@ -413,13 +422,7 @@ def run_batch(args, rank, world, dev):
     px = n_img * H * W
     # algorithmic FP32 ops of the whole batch (132 per pixel per
     # evaluated folded term); K per image from the host twin of the plan
-    ks = []
-    for f in imgs:
-        pl = P.select_plan(P.compute_T(f, R), p["sigma_r"], p["epsilon"])
-        ks.append(pl.N // 2 - pl.M + 1)
-    kt = torch.tensor([float(sum(ks))], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(kt)
+    kt = torch.tensor([float(sum(ks_all))], dtype=torch.float64)
     ops = OPS_PER_PX_TERM * H * W * float(kt.item())
     achieved = ops * args.steps / (total * 1e-3) / 1e12
     peak = 148 * 128 * 1.965e9 / 1e12
@@ -431,7 +434,8 @@ def run_batch(args, rank, world, dev):
                               ops_basis=f"{OPS_PER_PX_TERM} ops/px/term x {H}x{W} px x sum K = {int(kt.item())}"),
                 config=dict(workload=p["name"], images=n_img, H=H, W=W, sigma_s=p["sigma_s"],
                             sigma_r=p["sigma_r"], epsilon=p["epsilon"],
-                            parallelism=f"image batch sharded over {world} rank(s), no collective",
+                            parallelism=f"image batch sharded over {world} rank(s) by px*K (LPT), no collective",
+                            sum_K=int(sum(ks_all)), rank_K=[int(sum(ks_all[i] for i in part)) for part in parts],
                             l2="inputs (64 MiB/image) exceed what L2 keeps across images"))
 
 
