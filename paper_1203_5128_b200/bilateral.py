@@ -18,7 +18,7 @@ import numpy as np
 from . import _lib
 from .errors import InvalidParameterError
 from .image import stage
-from .kernels import KernelFamily, KernelPlan, log_2_over_eps, order_threshold, select_plan
+from .kernels import KernelFamily, KernelPlan, log_2_over_eps, select_plan
 from .maxfilter import _stream_ptr, local_range
 from .spatial import IteratedBox, SpatialMode, support_radius, to_c_spatial
 

@@ -1,5 +1,5 @@
 """Device time of the full pipeline per config (CUDA events), for triage."""
-import sys, os, time
+import sys, os
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1203_5128_b200 as P
