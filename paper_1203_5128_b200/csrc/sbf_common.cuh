@@ -84,6 +84,21 @@ int launch_plan(const double* T_dev, int use_fixed, double fixed_T, double sigma
                 int rule, double log_2_over_eps, sbf_plan* plan_dev, sbf_term* terms_dev,
                 int terms_cap, cudaStream_t st, int forced_N = 0, int forced_M = 0);
 
+// Stream-ordered device scratch that is released on every exit path
+// (cudaFreeAsync on the owning stream when it goes out of scope).
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  cudaStream_t st;
+  explicit DevBuf(cudaStream_t s) : st(s) {}
+  cudaError_t alloc(size_t n) { return cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), st); }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+
 struct FilterLaunch {
   const void* f;
   int dtype;

@@ -226,8 +226,9 @@ extern "C" int sbf_direct_bf_expansion(const void* f, int dtype, int64_t H, int6
     ht.freq[k] = freq[k];
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  DirectTerms* dt = nullptr;
-  SBF_CHECK_CUDA(cudaMallocAsync(&dt, sizeof(DirectTerms), st));
+  DevBuf<DirectTerms> dt_b(st);
+  SBF_CHECK_CUDA(dt_b.alloc(1));
+  DirectTerms* dt = dt_b.p;
   SBF_CHECK_CUDA(cudaMemcpyAsync(dt, &ht, sizeof(DirectTerms), cudaMemcpyHostToDevice, st));
   const dim3 block(32, 8), grid((unsigned)((W + 31) / 32), (unsigned)((H + 7) / 8));
 #define SBF_DT(FT, OT)                                                                        \
@@ -240,6 +241,5 @@ extern "C" int sbf_direct_bf_expansion(const void* f, int dtype, int64_t H, int6
 #undef SBF_DT
   SBF_CHECK_LAUNCH();
   // the pageable source was staged by cudaMemcpyAsync before it returned
-  SBF_CHECK_CUDA(cudaFreeAsync(dt, st));
   return SBF_OK;
 }

@@ -264,10 +264,11 @@ int launch_dual_direct(const FilterLaunch& a, const sbf_plan& plan) {
     else
       axis_row(a.W, x, a.sp.r, alpha, passes, S, hc.data() + x * T);
   }
-  double *Wr = nullptr, *Wc = nullptr;
-  double2* P = nullptr;
-  SBF_CHECK_CUDA(cudaMallocAsync(&Wr, sizeof(double) * hr.size(), st));
-  SBF_CHECK_CUDA(cudaMallocAsync(&Wc, sizeof(double) * hc.size(), st));
+  DevBuf<double> Wr_b(st), Wc_b(st);
+  DevBuf<double2> P_b(st);
+  SBF_CHECK_CUDA(Wr_b.alloc(hr.size()));
+  SBF_CHECK_CUDA(Wc_b.alloc(hc.size()));
+  double *Wr = Wr_b.p, *Wc = Wc_b.p;
   SBF_CHECK_CUDA(cudaMemcpyAsync(Wr, hr.data(), sizeof(double) * hr.size(),
                                  cudaMemcpyHostToDevice, st));
   SBF_CHECK_CUDA(cudaMemcpyAsync(Wc, hc.data(), sizeof(double) * hc.size(),
@@ -277,8 +278,9 @@ int launch_dual_direct(const FilterLaunch& a, const sbf_plan& plan) {
   const dim3 tb(32, 8), grid((unsigned)((a.W + 31) / 32), (unsigned)((rows_out + 7) / 8));
 
   // integer-valued image with a modest range: tabulated kernel
-  int* flag = nullptr;
-  SBF_CHECK_CUDA(cudaMallocAsync(&flag, sizeof(int), st));
+  DevBuf<int> flag_b(st);
+  SBF_CHECK_CUDA(flag_b.alloc(1));
+  int* flag = flag_b.p;
   SBF_CHECK_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
   if (a.dtype == SBF_F32)
     integral_check<float><<<gpix, 256, 0, st>>>(static_cast<const float*>(a.f), a.H, a.W, a.ld, flag);
@@ -291,12 +293,12 @@ int launch_dual_direct(const FilterLaunch& a, const sbf_plan& plan) {
   SBF_CHECK_CUDA(cudaMemcpyAsync(&non_integer, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   SBF_CHECK_CUDA(cudaMemcpyAsync(st_host, a.stats, sizeof(st_host), cudaMemcpyDeviceToHost, st));
   SBF_CHECK_CUDA(cudaStreamSynchronize(st));
-  SBF_CHECK_CUDA(cudaFreeAsync(flag, st));
   const double span = st_host[2] - st_host[1];
   if (!non_integer && span >= 0.0 && span <= 4194304.0) {
     const int64_t smax_v = (int64_t)span;
-    double* lut = nullptr;
-    SBF_CHECK_CUDA(cudaMallocAsync(&lut, sizeof(double) * (smax_v + 1), st));
+    DevBuf<double> lut_b(st);
+    SBF_CHECK_CUDA(lut_b.alloc(smax_v + 1));
+    double* lut = lut_b.p;
     kernel_table<<<(unsigned)smin<int64_t>((smax_v + 256) / 256, 148 * 8), 256, 0, st>>>(
         a.plan, smax_v, lut);
 #define SBF_DUAL_LUT(FT, OT)                                                                     \
@@ -315,12 +317,10 @@ int launch_dual_direct(const FilterLaunch& a, const sbf_plan& plan) {
     else SBF_DUAL_LUT(double, double);
 #undef SBF_DUAL_LUT
     SBF_CHECK_LAUNCH();
-    SBF_CHECK_CUDA(cudaFreeAsync(lut, st));
-    SBF_CHECK_CUDA(cudaFreeAsync(Wr, st));
-    SBF_CHECK_CUDA(cudaFreeAsync(Wc, st));
     return SBF_OK;
   }
-  SBF_CHECK_CUDA(cudaMallocAsync(&P, sizeof(double2) * a.H * a.W, st));
+  SBF_CHECK_CUDA(P_b.alloc((size_t)(a.H * a.W)));
+  double2* P = P_b.p;
 #define SBF_DUAL(FT, OT)                                                                         \
   do {                                                                                           \
     phasor_kernel<FT><<<gpix, 256, 0, st>>>(static_cast<const FT*>(a.f), a.H, a.W, a.ld, a.plan, \
@@ -335,9 +335,6 @@ int launch_dual_direct(const FilterLaunch& a, const sbf_plan& plan) {
   else SBF_DUAL(double, double);
 #undef SBF_DUAL
   SBF_CHECK_LAUNCH();
-  SBF_CHECK_CUDA(cudaFreeAsync(Wr, st));
-  SBF_CHECK_CUDA(cudaFreeAsync(Wc, st));
-  SBF_CHECK_CUDA(cudaFreeAsync(P, st));
   return SBF_OK;
 }
 

@@ -170,6 +170,7 @@ __global__ void gen_accum(const double* __restrict__ planes, const void* f, int 
 // ---- reusable fp64 smoother of four planes (also used by coarse NLM) ----
 int PlaneSmoother::init(const sbf_spatial& sp, int64_t H_, int64_t W_, int64_t row0_,
                         int64_t img_H_, cudaStream_t st) {
+  stream = st;
   H = H_;
   W = W_;
   row0 = row0_;
@@ -243,10 +244,11 @@ int launch_generic_terms(const FilterLaunch& a, double* nd) {
     SBF_CHECK_CUDA(cudaStreamSynchronize(st));
   }
   const int64_t H = a.H, W = a.W, n = H * W;
-  double* planes = nullptr;
-  double* tmp = nullptr;
-  SBF_CHECK_CUDA(cudaMallocAsync(&planes, sizeof(double) * 4 * n, st));
-  SBF_CHECK_CUDA(cudaMallocAsync(&tmp, sizeof(double) * 4 * n, st));
+  DevBuf<double> planes_b(st), tmp_b(st);
+  SBF_CHECK_CUDA(planes_b.alloc(4 * n));
+  SBF_CHECK_CUDA(tmp_b.alloc(4 * n));
+  double* planes = planes_b.p;
+  double* tmp = tmp_b.p;
   const int bs = 256;
   const unsigned gpix = (unsigned)smin<int64_t>((n + bs - 1) / bs, 148 * 16);
   PlaneSmoother sm;
@@ -266,9 +268,6 @@ int launch_generic_terms(const FilterLaunch& a, double* nd) {
                                    a.out_hi, a.stats, terms[k].turns, terms[k].scale, k == 0, nd);
     SBF_CHECK_LAUNCH();
   }
-  sm.release(st);
-  SBF_CHECK_CUDA(cudaFreeAsync(planes, st));
-  SBF_CHECK_CUDA(cudaFreeAsync(tmp, st));
   return SBF_OK;
 }
 

@@ -20,10 +20,15 @@ struct PlaneSmoother {
   const FusedEntry* fe = nullptr;
   double* gx = nullptr;
   double* gy = nullptr;
+  cudaStream_t stream = nullptr;
   int init(const sbf_spatial& sp, int64_t H, int64_t W, int64_t row0, int64_t img_H,
            cudaStream_t st);
   int run(double* planes, double* tmp, cudaStream_t st, int nplanes = 4) const;
   void release(cudaStream_t st);
+  PlaneSmoother() = default;
+  PlaneSmoother(const PlaneSmoother&) = delete;
+  PlaneSmoother& operator=(const PlaneSmoother&) = delete;
+  ~PlaneSmoother() { release(stream); }  // tables freed on every exit path
 };
 
 // Dual (direct) evaluation for untruncated plans (sbf_dual.cu): picked for

@@ -174,10 +174,11 @@ extern "C" int sbf_nlm_filter(const void* f, int dtype, int64_t H, int64_t W, in
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t n = H * W;
-  double *planes = nullptr, *tmp = nullptr, *nd = nullptr;
-  SBF_CHECK_CUDA(cudaMallocAsync(&planes, sizeof(double) * 4 * n, st));
-  SBF_CHECK_CUDA(cudaMallocAsync(&tmp, sizeof(double) * 4 * n, st));
-  SBF_CHECK_CUDA(cudaMallocAsync(&nd, sizeof(double) * 2 * n, st));
+  DevBuf<double> planes_b(st), tmp_b(st), nd_b(st);
+  SBF_CHECK_CUDA(planes_b.alloc(4 * n));
+  SBF_CHECK_CUDA(tmp_b.alloc(4 * n));
+  SBF_CHECK_CUDA(nd_b.alloc(2 * n));
+  double *planes = planes_b.p, *tmp = tmp_b.p, *nd = nd_b.p;
   PlaneSmoother sm;
   int rc = sm.init(*sp, H, W, 0, H, st);
   if (rc != SBF_OK) return rc;
@@ -204,10 +205,6 @@ extern "C" int sbf_nlm_filter(const void* f, int dtype, int64_t H, int64_t W, in
   else SBF_NLM_EPI(double, double);
 #undef SBF_NLM_EPI
   SBF_CHECK_LAUNCH();
-  sm.release(st);
-  SBF_CHECK_CUDA(cudaFreeAsync(planes, st));
-  SBF_CHECK_CUDA(cudaFreeAsync(tmp, st));
-  SBF_CHECK_CUDA(cudaFreeAsync(nd, st));
   return SBF_OK;
 }
 

@@ -66,9 +66,10 @@ extern "C" int sbf_smooth(const void* f, int dtype, int64_t H, int64_t W, int64_
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t n = H * W;
   const unsigned grid = (unsigned)smin<int64_t>((n + 255) / 256, 148 * 16);
-  double *a = nullptr, *b = nullptr;
-  SBF_CHECK_CUDA(cudaMallocAsync(&a, sizeof(double) * n, st));
-  SBF_CHECK_CUDA(cudaMallocAsync(&b, sizeof(double) * n, st));
+  DevBuf<double> a_b(st), b_b(st);
+  SBF_CHECK_CUDA(a_b.alloc(n));
+  SBF_CHECK_CUDA(b_b.alloc(n));
+  double *a = a_b.p, *b = b_b.p;
   double* res = a;
   if (sp->mode == SBF_SPATIAL_FIR) {
     SBF_REQUIRE(sp->sigma_s > 0.0 && sp->r >= 1, SBF_ERR_INVALID,
@@ -104,14 +105,11 @@ extern "C" int sbf_smooth(const void* f, int dtype, int64_t H, int64_t W, int64_
       rc = sm.run(a, b, st, 1);
       if (rc != SBF_OK) return rc;
     }
-    sm.release(st);
   }
   if (out_dtype == SBF_F64)
     store_plane<double><<<grid, 256, 0, st>>>(res, n, static_cast<double*>(out));
   else
     store_plane<float><<<grid, 256, 0, st>>>(res, n, static_cast<float*>(out));
   SBF_CHECK_LAUNCH();
-  SBF_CHECK_CUDA(cudaFreeAsync(a, st));
-  SBF_CHECK_CUDA(cudaFreeAsync(b, st));
   return SBF_OK;
 }
