@@ -32,9 +32,9 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-# our kernels per filtered image: stats init, row max, column max (+ stats
-# finalisation in its last CTA), plan, term sweep (K3), epilogue (K4)
-KERNELS_PER_IMAGE = 6
+# our kernels per filtered image: row max (+ statistics reset), column max
+# (+ statistics finalisation in its last CTA), plan, term sweep (K3), epilogue (K4)
+KERNELS_PER_IMAGE = 5
 METRIC = "Mpixel/s shiftable Gaussian BF at 1/2/4/8 B200; % of FP32/HBM roofline"
 UNIT = "Mpixel/s"
 OPS_PER_PX_TERM = 132   # phasor 4 + f*c,f*s 2 + 4 images x 6 line passes x 5 + acc 6
@@ -477,10 +477,10 @@ def run_strips(args, rank, world, dev):
     total = float(t.item())
     px = 3 * size * size
     plans = sf.plans_host()
-    # r >= 9 runs the split sweep: K1 (3) + plan + 2 kernels per term + K4
+    # r >= 9 runs the split sweep: K1 (2) + plan + 2 kernels per term + K4
     r_sp, _ = P.extended_box_params(p["sigma_s"], 3)
     if r_sp >= 9:
-        per_step = sum(4 + 2 * (pl.N // 2 - pl.M + 1) + 1 for pl in plans)
+        per_step = sum(3 + 2 * (pl.N // 2 - pl.M + 1) + 1 for pl in plans)
     else:
         per_step = KERNELS_PER_IMAGE * 3
     ops = OPS_PER_PX_TERM * size * size * sum(pl.N // 2 - pl.M + 1 for pl in plans)

@@ -25,9 +25,23 @@ template <typename T>
 __device__ __forceinline__ T vmax(T a, T b) { return a > b ? a : b; }
 
 // Row pass: out[y, x] = max f[y, clamp(x-R .. x+R)]
+__device__ __forceinline__ void init_stats(double* stats, unsigned* done) {
+  if (done) *done = 0u;
+  unsigned long long* red = reinterpret_cast<unsigned long long*>(stats + 4);
+  red[0] = ord_bits(0.0);
+  red[1] = ord_bits(INFINITY);
+  red[2] = ord_bits(-INFINITY);
+  red[3] = 0ull;  // non-finite sample count (stats[7], read as uint64)
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) rowmax_kernel(const T* __restrict__ f, int64_t W,
-                                                     int64_t ld, int R, T* __restrict__ out) {
+                                                     int64_t ld, int R, T* __restrict__ out,
+                                                     double* __restrict__ stats,
+                                                     unsigned* __restrict__ done) {
+  // the statistics accumulators are reset here (the column pass that updates
+  // them runs after this kernel on the stream): one launch fewer
+  if (stats && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) init_stats(stats, done);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* q = reinterpret_cast<T*>(smem_raw);
   const int64_t y = blockIdx.y;
@@ -220,14 +234,7 @@ __global__ void stats_only_kernel(const T* __restrict__ f, int64_t W, int64_t ld
   if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&red[3], bad);
 }
 
-__global__ void stats_init_kernel(double* stats, unsigned* done) {
-  if (done) *done = 0u;
-  unsigned long long* red = reinterpret_cast<unsigned long long*>(stats + 4);
-  red[0] = ord_bits(0.0);
-  red[1] = ord_bits(INFINITY);
-  red[2] = ord_bits(-INFINITY);
-  red[3] = 0ull;  // non-finite sample count (stats[7], read as uint64)
-}
+__global__ void stats_init_kernel(double* stats, unsigned* done) { init_stats(stats, done); }
 
 __global__ void stats_final_kernel(double* stats) { finalize_stats(stats); }
 
@@ -247,8 +254,10 @@ int run(const void* fv, int64_t H, int64_t W, int64_t ld, int R, int64_t t_lo, i
                 "local_range workspace too small");
     done = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + align_up((size_t)(H * W) * sizeof(T)));
   }
-  stats_init_kernel<<<1, 1, 0, st>>>(stats, done);
-  SBF_CHECK_LAUNCH();
+  if (R == 0) {
+    stats_init_kernel<<<1, 1, 0, st>>>(stats, done);
+    SBF_CHECK_LAUNCH();
+  }
   // a window wider than the image equals the image-wide window (clamping)
   const int Rr = (int)smin<int64_t>(R, smax<int64_t>(W - 1, 0));
   const int Rc = (int)smin<int64_t>(R, smax<int64_t>(H - 1, 0));
@@ -268,7 +277,7 @@ int run(const void* fv, int64_t H, int64_t W, int64_t ld, int R, int64_t t_lo, i
       SBF_CHECK_CUDA(cudaFuncSetAttribute(rowmax_kernel<T>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       dim3 grid((unsigned)((W + kRowSeg - 1) / kRowSeg), (unsigned)H);
-      rowmax_kernel<T><<<grid, 256, smem, st>>>(f, W, ld, Rr, rowmax);
+      rowmax_kernel<T><<<grid, 256, smem, st>>>(f, W, ld, Rr, rowmax, stats, done);
       SBF_CHECK_LAUNCH();
     }
     {
