@@ -263,6 +263,19 @@ int sbf_direct_nlm(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, i
 int sbf_smooth(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, const sbf_spatial* sp,
                void* out, int out_dtype, void* stream);
 
+/* ---- host -> device staging ----
+ * Copies n samples of page-locked (pinned) host memory `host_src` into device
+ * memory with the SMs reading over PCIe (faster than the copy engine for
+ * image-sized transfers); integer kinds are widened to float32 on the way
+ * (dev_dst float32), F32/F64 copy as is.  Stream-ordered; SBF_ERR_INVALID if
+ * host_src is not pinned host memory. */
+#define SBF_STAGE_F32 0
+#define SBF_STAGE_F64 1
+#define SBF_STAGE_U8 2
+#define SBF_STAGE_U16 3
+#define SBF_STAGE_I16 4
+int sbf_stage_h2d(const void* host_src, int src_kind, int64_t n, void* dev_dst, void* stream);
+
 /* ---- introspection / benchmarking hooks ---- */
 /* fp64 (HDR / generic) evaluation, this thread: 0 = always the K term sweeps,
  * 1 = cost model (default: the dual form cos(gamma s)^N over the (2S+1)^2

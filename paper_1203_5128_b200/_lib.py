@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("SBF_LIB", os.path.join(_HERE, "libsbf.so"))
 
 SBF_OK, SBF_ERR_INVALID, SBF_ERR_UNSUPPORTED, SBF_ERR_CUDA, SBF_ERR_WORKSPACE = 0, 2, 4, 5, 6
 SBF_F32, SBF_F64 = 0, 1
+STAGE_F32, STAGE_F64, STAGE_U8, STAGE_U16, STAGE_I16 = 0, 1, 2, 3, 4
 RULES = {"auto": 0, "exact": 1, "chernoff": 2, "none": 3}
 SPATIAL_ITERATED, SPATIAL_BOX, SPATIAL_FIR = 0, 1, 2
 PREC_FP32, PREC_HDR, PREC_AUTO = 0, 1, 2
@@ -87,6 +88,7 @@ _SIGS = {
     "sbf_direct_bf_expansion": (_int, [_vp, _int, _i64, _i64, _i64, _int, _vp, _vp, _vp, _int, _vp,
                                        _int, _vp]),
     "sbf_smooth": (_int, [_vp, _int, _i64, _i64, _i64, C.POINTER(SbfSpatial), _vp, _int, _vp]),
+    "sbf_stage_h2d": (_int, [_vp, _int, _i64, _vp, _vp]),
     "sbf_set_split_min_radius": (_int, [_int]),
     "sbf_nlm_filter": (_int, [_vp, _int, _i64, _i64, _i64, C.POINTER(SbfSpatial), _int, _vp, _vp,
                               _int, _vp, _vp, _int, _vp, _vp]),

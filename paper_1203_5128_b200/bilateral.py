@@ -9,6 +9,7 @@ GPU as K1 (local range) -> K2 (plan on device) -> K3 (fused term kernel)
 
 from __future__ import annotations
 
+import functools
 import warnings
 from dataclasses import dataclass
 from typing import NamedTuple, Optional
@@ -19,7 +20,7 @@ from . import _lib
 from .errors import InvalidParameterError
 from .image import stage
 from .kernels import KernelFamily, KernelPlan, log_2_over_eps, select_plan
-from .maxfilter import _stream_ptr, local_range
+from .maxfilter import _stream_ptr
 from .spatial import IteratedBox, SpatialMode, support_radius, to_c_spatial
 
 TERMS_CAP = 1 << 16
@@ -112,76 +113,86 @@ def shiftable_bf(img, params: FilterParams) -> ShiftableResult:
     return ShiftableResult(result, plan, fallbacks)
 
 
+# device "meta" block of one call: plan | fallback counter | statistics, read
+# back with a single copy
+_META_PLAN, _META_FB, _META_STATS, _META_BYTES = 0, 64, 128, 256
+
+
+@functools.lru_cache(maxsize=64)
+def _workspace_layout(H, W, dtype, sp_key, prec):
+    """(total bytes, term-table offset, filter-workspace offset) of the
+    sbf_shiftable_bf workspace: [K1 workspace | term table | K3/K4 workspace]."""
+    lib = _lib.load()
+    sp = _lib.SbfSpatial(*sp_key)
+    total = lib.sbf_shiftable_bf_workspace(H, W, dtype, sp, prec, TERMS_CAP)
+    terms_off = lib.sbf_local_range_workspace(H, W, dtype)
+    return max(total, 256), terms_off, terms_off + ((TERMS_CAP * 32 + 255) // 256) * 256
+
+
 def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False):
     """K1..K4 on a staged device image; returns (output, KernelPlan, fallbacks).
 
-    The pipeline runs without a host round trip and synchronises once at the
-    end (non-finite input is rejected after the fact); "auto" resolves fp32
-    vs HDR on the device and re-runs the fp64 path only for wide ranges.
-    `to_host` copies the result into pinned host memory (cached allocator).
+    One C call (sbf_shiftable_bf) launches the whole pipeline without a host
+    round trip; the call synchronises once at the end on a single read-back of
+    plan, fallback count and statistics (non-finite input is rejected after
+    the fact).  "auto" resolves fp32 vs HDR on the device and re-runs the fp64
+    path only for wide ranges.  `to_host` copies the result into pinned host
+    memory (cached allocator).
     """
     import torch
 
     if params.family is KernelFamily.POLYNOMIAL:
         raise InvalidParameterError("the polynomial family is not supported by the CUDA path")
     lib = _lib.load()
-    mode = params.resolved_spatial()
-    sp = to_c_spatial(mode)
+    sp = to_c_spatial(params.resolved_spatial())
     radius = params.resolved_radius()
     dev = s.tensor.device
     H, W = s.H, s.W
     use_fixed = params.fixed_T is not None
-    # K1: T (or only the statistics when T is fixed)
-    stats, _ = local_range(s, 0 if use_fixed else radius)
+    if use_fixed and not float(params.fixed_T) >= 0.0:
+        raise InvalidParameterError("T must be non-negative")  # kernels.py:118-119
     prec = _precision_code(params)
     stream = _stream_ptr()
-    plan_dev = torch.empty(64, dtype=torch.uint8, device=dev)
-    terms = torch.empty(TERMS_CAP * 32, dtype=torch.uint8, device=dev)
-    def plan_on_device(forced=None):
-        args = (stats.data_ptr(), 1 if use_fixed else 0,
-                float(params.fixed_T) if use_fixed else 0.0, float(params.sigma_r),
-                float(params.epsilon), _lib.RULES.get(params.truncation, -1),
-                log_2_over_eps(params.epsilon))
-        if forced is None:
-            _lib.check(lib.sbf_plan_device(*args, plan_dev.data_ptr(), terms.data_ptr(),
-                                           TERMS_CAP, stream), "plan")
-        else:
-            _lib.check(lib.sbf_plan_device_forced(*args, forced[0], forced[1], plan_dev.data_ptr(),
-                                                  terms.data_ptr(), TERMS_CAP, stream), "plan")
-
-    plan_on_device()
-    out_dtype = _lib.SBF_F64 if out_f64 else _lib.SBF_F32
+    rule = _lib.RULES.get(params.truncation, -1)
+    l2e = log_2_over_eps(params.epsilon)
+    total, terms_off, fws_off = _workspace_layout(
+        H, W, s.dtype, (sp.mode, sp.passes, sp.r, 0, sp.alpha, sp.sigma_s), prec)
+    meta = torch.zeros(_META_BYTES, dtype=torch.uint8, device=dev)
+    ws = torch.empty(total, dtype=torch.uint8, device=dev)
+    plan_ptr = meta.data_ptr() + _META_PLAN
+    fb_ptr = meta.data_ptr() + _META_FB
+    stats_ptr = meta.data_ptr() + _META_STATS
+    terms_ptr = ws.data_ptr() + terms_off
     out = torch.empty((H, W), dtype=torch.float64 if out_f64 else torch.float32, device=dev)
-    fb = torch.zeros(1, dtype=torch.int64, device=dev)
-    ws_bytes = lib.sbf_filter_workspace(H, W, H, s.dtype, sp, prec)
-    ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dev)
-    _lib.check(lib.sbf_filter(s.tensor.data_ptr(), s.dtype, H, W, W, 0, H, 0, H, sp,
-                              plan_dev.data_ptr(), terms.data_ptr(), stats.data_ptr(), prec,
-                              out.data_ptr(), out_dtype, fb.data_ptr(), ws.data_ptr(), ws.numel(),
-                              stream), "filter")
+    out_dtype = _lib.SBF_F64 if out_f64 else _lib.SBF_F32
+    _lib.check(lib.sbf_shiftable_bf(s.tensor.data_ptr(), s.dtype, H, W, sp, radius,
+                                    float(params.fixed_T) if use_fixed else -1.0,
+                                    float(params.sigma_r), float(params.epsilon), rule, l2e, prec,
+                                    out.data_ptr(), out_dtype, plan_ptr, stats_ptr, fb_ptr,
+                                    TERMS_CAP, ws.data_ptr(), total, stream), "shiftable_bf")
     out_dev = out
     if to_host:
         host = torch.empty((H, W), dtype=out.dtype, pin_memory=True)
         host.copy_(out, non_blocking=True)
         out = host
-    # one small read-back for plan, fallback count and the input check
-    tail = torch.cat([plan_dev, fb.view(torch.uint8), stats.view(torch.uint8)]).cpu().numpy()
-    plan_c = _lib.SbfPlan.from_buffer_copy(tail[:64].tobytes())
-    fallbacks = int(tail[64:72].view(np.int64)[0])
-    if int(tail[72:].view(np.uint64)[7]) != 0:
+    tail = meta.cpu().numpy()
+    stats_host = tail[_META_STATS:_META_STATS + 64]
+    if int(stats_host.view(np.uint64)[7]) != 0:
         raise InvalidParameterError("image contains non-finite samples")
+    plan_c = _lib.SbfPlan.from_buffer_copy(tail[_META_PLAN:_META_PLAN + 64].tobytes())
     _lib.check(plan_c.status, "plan")
+    fallbacks = int(tail[_META_FB:_META_FB + 8].view(np.int64)[0])
 
     def rerun():
-        fb.zero_()
-        _lib.check(lib.sbf_filter(s.tensor.data_ptr(), s.dtype, H, W, W, 0, H, 0, H, sp,
-                                  plan_dev.data_ptr(), terms.data_ptr(), stats.data_ptr(),
-                                  prec, out_dev.data_ptr(), out_dtype, fb.data_ptr(),
-                                  ws.data_ptr(), ws.numel(), stream), "filter")
+        meta[_META_FB:_META_FB + 8].zero_()
+        _lib.check(lib.sbf_filter(s.tensor.data_ptr(), s.dtype, H, W, W, 0, H, 0, H, sp, plan_ptr,
+                                  terms_ptr, stats_ptr, prec, out_dev.data_ptr(), out_dtype, fb_ptr,
+                                  ws.data_ptr() + fws_off, total - fws_off, stream), "filter")
         if to_host:
             out.copy_(out_dev)
-        return (_lib.SbfPlan.from_buffer_copy(plan_dev.cpu().numpy().tobytes()),
-                int(fb.item()))
+        t = meta.cpu().numpy()
+        return (_lib.SbfPlan.from_buffer_copy(t[_META_PLAN:_META_PLAN + 64].tobytes()),
+                int(t[_META_FB:_META_FB + 8].view(np.int64)[0]))
 
     if plan_c.flags & _lib.PLAN_NEEDS_HDR:
         # the device guard found |f - centre| > 4096: fp64 path
@@ -192,7 +203,11 @@ def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False
         # (libm pow, bit-equal to CPython) decides, and the filter is re-run
         ph = select_plan(plan_c.T, params.sigma_r, params.epsilon, truncation=params.truncation)
         if (ph.N, ph.M) != (plan_c.N, plan_c.M):
-            plan_on_device(forced=(ph.N, ph.M))
+            _lib.check(lib.sbf_plan_device_forced(stats_ptr, 1 if use_fixed else 0,
+                                                  float(params.fixed_T) if use_fixed else 0.0,
+                                                  float(params.sigma_r), float(params.epsilon),
+                                                  rule, l2e, ph.N, ph.M, plan_ptr, terms_ptr,
+                                                  TERMS_CAP, stream), "plan")
             plan_c, fallbacks = rerun()
     return out, _plan_from_struct(plan_c), fallbacks
 

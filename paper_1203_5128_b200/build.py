@@ -27,7 +27,7 @@ FLAGS = ["-O3", "-lineinfo", "-Xptxas", "-warn-spills", "-std=c++17", "-Xcompile
          "-I", INCLUDE, "-I", CSRC]
 
 SOURCES = ["sbf_api.cu", "sbf_plan.cu", "sbf_local_range.cu", "sbf_generic.cu", "sbf_pgm.cu",
-           "sbf_direct.cu", "sbf_nlm.cu", "sbf_dual.cu", "sbf_smooth.cu"]
+           "sbf_direct.cu", "sbf_nlm.cu", "sbf_dual.cu", "sbf_smooth.cu", "sbf_stage.cu"]
 
 
 def instantiations(kind: str):

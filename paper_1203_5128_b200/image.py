@@ -57,6 +57,44 @@ class Staged:
     torch_in: bool = False  # caller passed a torch tensor (results keep its float dtype)
 
 
+def _stage_kinds():
+    import torch
+
+    kinds = {torch.float32: _lib.STAGE_F32, torch.float64: _lib.STAGE_F64,
+             torch.uint8: _lib.STAGE_U8, torch.int16: _lib.STAGE_I16}
+    if hasattr(torch, "uint16"):
+        kinds[torch.uint16] = _lib.STAGE_U16
+    return kinds
+
+
+class _Kinds(dict):
+    """dtype -> sbf_stage_h2d source kind, filled on first use (lazy torch)."""
+
+    def __contains__(self, k):
+        if not len(self):
+            self.update(_stage_kinds())
+        return dict.__contains__(self, k)
+
+
+_STAGE_KINDS = _Kinds()
+
+
+def _stage_pinned(t, device=None):
+    """Pinned contiguous host tensor -> CUDA tensor via sbf_stage_h2d."""
+    import torch
+
+    kind = _STAGE_KINDS[t.dtype]
+    out_dtype = torch.float64 if kind == _lib.STAGE_F64 else torch.float32
+    dev = torch.empty(tuple(t.shape), dtype=out_dtype, device=device or "cuda")
+    with torch.cuda.device(dev.device):
+        stream = torch.cuda.current_stream().cuda_stream
+        _lib.check(_lib.load().sbf_stage_h2d(t.data_ptr(), kind, t.numel(), dev.data_ptr(), stream),
+                   "stage_h2d")
+    # the read is stream-ordered; every public entry point synchronises on its
+    # result before returning, so `t` outlives it
+    return dev
+
+
 def stage(img, device=None) -> Staged:
     """Put `img` (numpy array, torch tensor or nested sequence) on the GPU."""
     import torch
@@ -68,11 +106,14 @@ def stage(img, device=None) -> Staged:
         if t.numel() == 0:
             raise InvalidParameterError("image must be non-empty")
         host = not t.is_cuda
-        if t.dtype not in (torch.float32, torch.float64):
+        if host and t.is_pinned() and t.is_contiguous() and t.dtype in _STAGE_KINDS:
+            # pinned sources: the SMs read them over PCIe (sbf_stage_h2d),
+            # stream-ordered before K1; 8/16-bit samples widen on the device
+            t = _stage_pinned(t, device)
+        elif t.dtype not in (torch.float32, torch.float64):
             exact32 = t.dtype in (torch.uint8, torch.int8, torch.int16, torch.bool)
             t = t.to(torch.float32 if exact32 else torch.float64)
-        if host:
-            # pinned sources copy asynchronously, ordered before K1 on the stream
+        if host and not t.is_cuda:
             t = t.contiguous().to(device or "cuda", non_blocking=t.is_pinned())
         t = t.contiguous()
     else:
