@@ -161,7 +161,9 @@ size_t sbf_filter_workspace(int64_t H, int64_t W, int64_t rows_out, int dtype,
  * holding global image rows [row0, row0 + H) of an image of global height
  * img_H (border renormalisation only at true image borders).  The buffer
  * must include every row within the spatial support of the output rows.
- * out: (out_hi - out_lo) x W, pitch W, dtype out_dtype.
+ * out: (out_hi - out_lo) x W, pitch W, dtype out_dtype; device memory or
+ * page-locked host memory (then written by the device over PCIe: on the K3
+ * path segment by segment while the last terms run -- no separate copy).
  * stats_dev: from sbf_local_range ([3] = centre).  fallback_dev: one
  * unsigned long long counter (accumulated). */
 int sbf_filter(const void* f, int dtype, int64_t H, int64_t W, int64_t ld,
@@ -291,6 +293,12 @@ int sbf_filter_geometry(int64_t rows_out, int64_t W, const sbf_spatial* sp, int 
                         int* out7);
 int sbf_truncation_index_exact_bigint(int N, double epsilon, int* M);
 int sbf_set_stage_mask(int mask);
+/* K3 path, this thread: the divide/fallback epilogue streamed behind the term
+ * kernel (programmatic dependent launch; each output segment is divided out
+ * -- and, for a page-locked host output, written over PCIe -- as soon as
+ * every term has landed on it): 1 (default) = when out is host memory,
+ * 2 = always, 0 = never.  Returns the previous setting (-1: bad mode). */
+int sbf_set_fused_epilogue(int mode);
 int sbf_fp32_probe(int blocks, int threads, int iters, float* out_dev, void* stream);
 
 #ifdef __cplusplus

@@ -136,8 +136,8 @@ def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False
     round trip; the call synchronises once at the end on a single read-back of
     plan, fallback count and statistics (non-finite input is rejected after
     the fact).  "auto" resolves fp32 vs HDR on the device and re-runs the fp64
-    path only for wide ranges.  `to_host` copies the result into pinned host
-    memory (cached allocator).
+    path only for wide ranges.  `to_host`: the result lands in page-locked
+    host memory (cached allocator), written by the device directly.
     """
     import torch
 
@@ -163,18 +163,16 @@ def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False
     fb_ptr = meta.data_ptr() + _META_FB
     stats_ptr = meta.data_ptr() + _META_STATS
     terms_ptr = ws.data_ptr() + terms_off
-    out = torch.empty((H, W), dtype=torch.float64 if out_f64 else torch.float32, device=dev)
+    # host results are written by the epilogue straight into page-locked
+    # memory over PCIe (segment by segment, while the last terms still run)
+    out = torch.empty((H, W), dtype=torch.float64 if out_f64 else torch.float32,
+                      **({"pin_memory": True} if to_host else {"device": dev}))
     out_dtype = _lib.SBF_F64 if out_f64 else _lib.SBF_F32
     _lib.check(lib.sbf_shiftable_bf(s.tensor.data_ptr(), s.dtype, H, W, sp, radius,
                                     float(params.fixed_T) if use_fixed else -1.0,
                                     float(params.sigma_r), float(params.epsilon), rule, l2e, prec,
                                     out.data_ptr(), out_dtype, plan_ptr, stats_ptr, fb_ptr,
                                     TERMS_CAP, ws.data_ptr(), total, stream), "shiftable_bf")
-    out_dev = out
-    if to_host:
-        host = torch.empty((H, W), dtype=out.dtype, pin_memory=True)
-        host.copy_(out, non_blocking=True)
-        out = host
     tail = meta.cpu().numpy()
     stats_host = tail[_META_STATS:_META_STATS + 64]
     if int(stats_host.view(np.uint64)[7]) != 0:
@@ -186,10 +184,8 @@ def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False
     def rerun():
         meta[_META_FB:_META_FB + 8].zero_()
         _lib.check(lib.sbf_filter(s.tensor.data_ptr(), s.dtype, H, W, W, 0, H, 0, H, sp, plan_ptr,
-                                  terms_ptr, stats_ptr, prec, out_dev.data_ptr(), out_dtype, fb_ptr,
+                                  terms_ptr, stats_ptr, prec, out.data_ptr(), out_dtype, fb_ptr,
                                   ws.data_ptr() + fws_off, total - fws_off, stream), "filter")
-        if to_host:
-            out.copy_(out_dev)
         t = meta.cpu().numpy()
         return (_lib.SbfPlan.from_buffer_copy(t[_META_PLAN:_META_PLAN + 64].tobytes()),
                 int(t[_META_FB:_META_FB + 8].view(np.int64)[0]))

@@ -112,6 +112,10 @@ static bool spatial_coeffs(const sbf_spatial& sp, int* r, int* passes, double* a
          *passes >= 1 && *alpha >= 0.0 && *alpha < 1.0;
 }
 
+// K3 control block: [queue head, epilogue queue head, pad..16 ints, one
+// counter per output segment (at most one per row)]
+static size_t terms_ctrl_bytes(int64_t rows_out) { return align_up((size_t)(rows_out + 16) * 4); }
+
 // partial accumulators (+ an fp32 centred copy of float64 inputs for K3)
 size_t filter_ws(int64_t H, int64_t W, int64_t rows_out, int dtype, const sbf_spatial* sp,
                  int precision) {
@@ -128,7 +132,8 @@ size_t filter_ws(int64_t H, int64_t W, int64_t rows_out, int dtype, const sbf_sp
   if (!e) return align_up((size_t)(rows_out * W) * 16);  // generic: one fp64 accumulator
   TermGeom g;
   choose_geometry(*e, rows_out, W, &g);
-  size_t bytes = align_up((size_t)(rows_out * W) * 8) + 256;  // accumulator + queue head
+  // accumulator + queue heads and per-segment counters of the fused epilogue
+  size_t bytes = align_up((size_t)(rows_out * W) * 8) + terms_ctrl_bytes(rows_out);
   if (dtype == SBF_F64) bytes += align_up((size_t)(H * W) * 4);
   return bytes;
 }
@@ -176,6 +181,153 @@ __global__ void epilogue_kernel(const ACC* __restrict__ nd, int groups, int64_t 
   if ((threadIdx.x & 31) == 0 && bad_count) atomicAdd(fallback, bad_count);
 }
 
+// ------------------- K4, streamed behind K3 (K3 path) -------------------
+// Launched programmatically dependent on K3 (which triggers at its start), so
+// its two-warp CTAs take whatever room K3 leaves on the SMs and
+// the rest start as K3 CTAs retire.  CTAs pull chunks of output rows in
+// segment order, wait until every K3 item of the chunk's segment has landed
+// (K3 bumps per-segment counters after a fence), and apply K4's arithmetic;
+// a page-locked host `out` is thereby written over PCIe while the last
+// terms are still being swept.
+struct StreamEpi {
+  const float2* nd;
+  const void* fo;
+  void* out;
+  const double* stats;
+  sbf_plan* plan;
+  unsigned long long* fallback;
+  int* ctrl;  // K3 control block: [1] chunk queue, [2..7] schedule, [8] ready, [16..] segments
+  int64_t fo_ld;
+  int W, rows_all, out_lo, nstrips, fo_dtype, out_dtype;
+};
+
+constexpr int kEpiThreads = 64;
+constexpr int kEpiPx = 4096;  // pixels per chunk
+constexpr long long kEpiTimeout = 1ll << 33;  // cycles (~4 s): only a failed K3 gets here
+
+// <= 64 registers: two warps fit in the 4096 registers a 2-CTA K3 (240 regs) leaves
+__global__ void __launch_bounds__(kEpiThreads, 16) stream_epilogue_kernel(const StreamEpi e) {
+  __shared__ int s_c, s_ok;
+  volatile int* vc = e.ctrl;
+  if (threadIdx.x == 0) {
+    // K3's schedule, or its early exit (plan error / HDR guard)
+    int ok = 1;
+    const long long t0 = clock64();
+    while (vc[8] == 0) {
+      const int status = *reinterpret_cast<volatile int*>(&e.plan->status);
+      const int flags = *reinterpret_cast<volatile int*>(&e.plan->flags);
+      if (status != SBF_OK || (flags & SBF_PLAN_NEEDS_HDR)) { ok = 0; break; }
+      if (clock64() - t0 > kEpiTimeout) {
+        atomicCAS(&e.plan->status, SBF_OK, SBF_ERR_CUDA);
+        ok = 0;
+        break;
+      }
+      __nanosleep(256);
+    }
+    __threadfence();
+    s_ok = ok;
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  const int seg_h = vc[2], nsegs = vc[3], bandh = vc[4], bandh_s = vc[5], Ks = vc[6], K_eval = vc[7];
+  const int chunk_rows = max(1, min(seg_h, kEpiPx / max(e.W, 1)));
+  const int cps = (seg_h + chunk_rows - 1) / chunk_rows;
+  const int n_chunks = nsegs * cps;
+  const double center = e.stats[3];
+  const float cf = (float)center;
+  unsigned long long bad_count = 0;
+  const bool vec = e.out_dtype == SBF_F32 && e.fo_dtype == SBF_F32 && (e.W & 3) == 0 &&
+                   (e.fo_ld & 3) == 0 && (reinterpret_cast<uintptr_t>(e.fo) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(e.out) & 15) == 0;
+  for (;;) {
+    if (threadIdx.x == 0) s_c = atomicAdd(e.ctrl + 1, 1);
+    __syncthreads();
+    const int c = s_c;
+    if (c >= n_chunks) break;
+    const int seg = c / cps;
+    const int ys0 = seg * seg_h, ys1 = min(e.rows_all, ys0 + seg_h);
+    const int r0 = ys0 + (c - seg * cps) * chunk_rows, r1 = min(r0 + chunk_rows, ys1);
+    if (threadIdx.x == 0) {
+      const int nm = (ys1 - 1) / bandh - ys0 / bandh + 1;
+      const int nt = Ks > 0 ? (ys1 - 1) / bandh_s - ys0 / bandh_s + 1 : 0;
+      const int expected = e.nstrips * ((K_eval - Ks) * nm + Ks * nt);
+      const long long t0 = clock64();
+      while (vc[16 + seg] < expected) {
+        if (clock64() - t0 > kEpiTimeout) {
+          atomicCAS(&e.plan->status, SBF_OK, SBF_ERR_CUDA);
+          break;
+        }
+        __nanosleep(256);
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    if (r0 < r1 && vec) {
+      // 4 pixels per quad, 4 quads in flight per thread
+      const int qw = e.W >> 2;
+      const int nq = (r1 - r0) * qw;
+      const float4* nd4 = reinterpret_cast<const float4*>(e.nd);
+      for (int q0 = threadIdx.x; q0 < nq; q0 += 4 * kEpiThreads) {
+        float4 a[4], b[4], fv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int q = q0 + u * kEpiThreads;
+          if (q < nq) {
+            const int y = r0 + q / qw, xq = q - (q / qw) * qw;
+            const int64_t i4 = (int64_t)y * qw + xq;
+            a[u] = __ldcg(nd4 + 2 * i4);
+            b[u] = __ldcg(nd4 + 2 * i4 + 1);
+            fv[u] = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(e.fo) +
+                                                          (int64_t)(e.out_lo + y) * e.fo_ld) + xq);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int q = q0 + u * kEpiThreads;
+          if (q < nq) {
+            const int y = r0 + q / qw, xq = q - (q / qw) * qw;
+            const bool b0 = !(a[u].y > 0.f), b1 = !(a[u].w > 0.f), b2 = !(b[u].y > 0.f),
+                       b3 = !(b[u].w > 0.f);
+            float4 o;
+            o.x = b0 ? fv[u].x : a[u].x / a[u].y + cf;
+            o.y = b1 ? fv[u].y : a[u].z / a[u].w + cf;
+            o.z = b2 ? fv[u].z : b[u].x / b[u].y + cf;
+            o.w = b3 ? fv[u].w : b[u].z / b[u].w + cf;
+            bad_count += (unsigned)b0 + (unsigned)b1 + (unsigned)b2 + (unsigned)b3;
+            reinterpret_cast<float4*>(e.out)[(int64_t)y * qw + xq] = o;
+          }
+        }
+      }
+    } else {
+      for (int y = r0; y < r1; ++y) {
+        const int64_t fy = (int64_t)(e.out_lo + y) * e.fo_ld;
+        for (int x = threadIdx.x; x < e.W; x += kEpiThreads) {
+          const int64_t i = (int64_t)y * e.W + x;
+          const float2 v = __ldcg(e.nd + i);
+          // K4's arithmetic: fp32 when the output is fp32
+          if (e.out_dtype == SBF_F32) {
+            const bool bad = !(v.y > 0.f);
+            const float fv = e.fo_dtype == SBF_F32 ? static_cast<const float*>(e.fo)[fy + x]
+                                                   : (float)static_cast<const double*>(e.fo)[fy + x];
+            static_cast<float*>(e.out)[i] = bad ? fv : v.x / v.y + cf;
+            bad_count += bad;
+          } else {
+            const double num = v.x, den = v.y;
+            const bool bad = !(den > 0.0);
+            const double fv = e.fo_dtype == SBF_F32 ? (double)static_cast<const float*>(e.fo)[fy + x]
+                                                    : static_cast<const double*>(e.fo)[fy + x];
+            static_cast<double*>(e.out)[i] = bad ? fv : num / den + center;
+            bad_count += bad;
+          }
+        }
+      }
+    }
+    __syncthreads();  // s_c is rewritten next round
+  }
+  for (int o = 16; o; o >>= 1) bad_count += __shfl_xor_sync(0xffffffffu, bad_count, o);
+  if ((threadIdx.x & 31) == 0 && bad_count) atomicAdd(e.fallback, bad_count);
+}
+
 template <typename ACC>
 static int launch_epilogue(const FilterLaunch& a, const ACC* nd, int groups, int64_t gstride) {
   const int64_t rows = a.out_hi - a.out_lo;
@@ -199,6 +351,10 @@ static thread_local int g_stage_mask = 3;
 // fp64 evaluation choice: 0 = always the term sweeps, 1 = cost model, 2 = dual
 // whenever exact (M = 0)
 static thread_local int g_dual_mode = 1;
+// K4 streamed behind K3 (programmatic dependent launch, per-segment
+// completion counters): 1 = when the output is page-locked host memory,
+// 2 = always, 0 = never (plain epilogue launch)
+static thread_local int g_fused_epi = 1;
 // set while an SBF_PREC_AUTO call runs the guarded fp32 term kernel
 static thread_local int g_hdr_guard = 0;
 
@@ -332,7 +488,7 @@ int launch_filter(const FilterLaunch& a) {
   }
   TermGeom g;
   choose_geometry(*e, rows_out, a.W, &g);
-  const size_t nd_bytes = align_up((size_t)(rows_out * a.W) * 8) + 256;
+  const size_t nd_bytes = align_up((size_t)(rows_out * a.W) * 8) + terms_ctrl_bytes(rows_out);
   const size_t need = filter_ws(a.H, a.W, rows_out, a.dtype, &a.sp, a.precision);
   SBF_REQUIRE(a.ws && a.ws_bytes >= need, SBF_ERR_WORKSPACE,
               "filter workspace too small (%zu < %zu)", a.ws_bytes, need);
@@ -372,8 +528,22 @@ int launch_filter(const FilterLaunch& a) {
   p.stats = a.stats;
   p.nd = a.ws;
   p.nd_group_stride = rows_out * a.W;
-  p.counter = reinterpret_cast<int*>(static_cast<char*>(a.ws) + nd_bytes - 256);
+  int* ctrl = reinterpret_cast<int*>(static_cast<char*>(a.ws) + nd_bytes - terms_ctrl_bytes(rows_out));
+  p.counter = ctrl;
   p.hdr_guard = g_hdr_guard;
+  // K4 streamed behind K3 when the output goes to page-locked host memory
+  // (its PCIe writes then overlap the sweep); device outputs take the plain
+  // epilogue launch, which is faster there (measured 464 vs 489 us, config 2)
+  bool out_host = false;
+  if (g_fused_epi == 1) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, a.out) == cudaSuccess)
+      out_host = at.type == cudaMemoryTypeHost;
+    else
+      cudaGetLastError();
+  }
+  p.epi = (g_stage_mask & 3) == 3 && (g_fused_epi == 2 || out_host);
+  p.seg_done = ctrl + 16;
   if (g_stage_mask & 1) {
     SBF_CHECK_CUDA(cudaMemsetAsync(a.ws, 0, nd_bytes, a.stream));
   }
@@ -382,7 +552,35 @@ int launch_filter(const FilterLaunch& a) {
     if (rc != SBF_OK) return rc;
   }
   if (!(g_stage_mask & 2)) return SBF_OK;
-  return launch_epilogue<float>(a, static_cast<const float*>(a.ws), g.groups, rows_out * a.W);
+  if (!p.epi)
+    return launch_epilogue<float>(a, static_cast<const float*>(a.ws), g.groups, rows_out * a.W);
+  StreamEpi ep;
+  ep.nd = static_cast<const float2*>(a.ws);
+  ep.fo = a.f;
+  ep.out = a.out;
+  ep.stats = a.stats;
+  ep.plan = const_cast<sbf_plan*>(a.plan);
+  ep.fallback = a.fallback;
+  ep.ctrl = ctrl;
+  ep.fo_ld = a.ld;
+  ep.W = (int)a.W;
+  ep.rows_all = (int)rows_out;
+  ep.out_lo = (int)a.out_lo;
+  ep.nstrips = p.nstrips;
+  ep.fo_dtype = a.dtype;
+  ep.out_dtype = a.out_dtype;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(sm_count() * 8));
+  cfg.blockDim = dim3(kEpiThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = a.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SBF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, stream_epilogue_kernel, ep));
+  return SBF_OK;
 }
 
 }  // namespace sbf
@@ -397,6 +595,13 @@ int sbf_abi_version(void) { return SBF_ABI_VERSION; }
 
 // Benchmark hook: restrict sbf_filter to the term kernel (1), the epilogue
 // (2) or both (3, default) on the calling thread.
+int sbf_set_fused_epilogue(int on) {
+  const int prev = sbf::g_fused_epi;
+  if (on < 0 || on > 2) return -1;
+  sbf::g_fused_epi = on;
+  return prev;
+}
+
 int sbf_set_stage_mask(int mask) {
   if (mask < 1 || mask > 3) return SBF_ERR_INVALID;
   sbf::g_stage_mask = mask;

@@ -61,6 +61,11 @@ struct TermParams {
   void* nd;
   int64_t nd_group_stride;  // (num, den) pairs per group
   int hdr_guard;            // SBF_PREC_AUTO: bail out (flag the plan) on wide ranges
+  // streamed epilogue (epi != 0): K3 publishes its segment schedule and
+  // per-segment item counts; the epilogue kernel divides segments out as
+  // soon as they are complete (stream_epilogue_kernel, sbf_api.cu)
+  int epi;
+  int* seg_done;  // per output segment: finished items (zeroed before launch)
 };
 
 // SBF_PREC_AUTO guard: the fp32 kernels are accurate to the north-star
@@ -88,8 +93,17 @@ __device__ __forceinline__ bool needs_hdr(const double* stats) {
 #ifndef SBF_TAIL_FRAC
 #define SBF_TAIL_FRAC 4   // at most K/4 terms in the tail
 #endif
-#ifndef SBF_TAIL2
-#define SBF_TAIL2 0  // last tail terms in half-height bands again (measured: slower)
+#ifndef SBF_PDL_TRIGGER
+#define SBF_PDL_TRIGGER 1  // let the streamed epilogue launch while K3 runs
+#endif
+#ifndef SBF_EPI_COUNTERS
+#define SBF_EPI_COUNTERS 1  // per-segment completion counters (streamed epilogue)
+#endif
+#ifndef SBF_MAIN_BAND_MAJOR
+#define SBF_MAIN_BAND_MAJOR 1  // main items band by band (output segments complete early)
+#endif
+#ifndef SBF_TAIL_BAND_MAJOR
+#define SBF_TAIL_BAND_MAJOR 1  // tail items band by band
 #endif
 #ifndef SBF_H_FIXED_SEQ
 #define SBF_H_FIXED_SEQ 1  // interior strips: warm-up / main-loop / tail H blocks, no dispatch
@@ -257,6 +271,11 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
   float* gh = gv + gv_len;
   float* FR = gh + HALO_W + GOFF;  // per-thread ring of prefetched f samples (L slots)
 
+  // the streamed epilogue (launched programmatically dependent) may start
+  // now: its CTAs take whatever SM room K3 leaves and wait for segments
+#if SBF_PDL_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   const sbf_plan* plan = p.plan;
   if (plan->status != SBF_OK) return;
   if (p.hdr_guard && needs_hdr(p.stats)) {
@@ -289,17 +308,27 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
     Ks = min(K_eval / SBF_TAIL_FRAC, (SBF_TAIL_WAVES * (int)gridDim.x + units_s - 1) / units_s);
   }
   const int bandh_s = (rows_all + bands_s - 1) / bands_s;
-  // the very last terms of the tail in bands half as tall again
-  int Ks2 = 0, bands_s2 = 1, units_s2 = 0;
-  if (SBF_TAIL2 && Ks >= 2 && bandh_s >= 2 * 4 * HALO) {
-    bands_s2 = 2 * bands_s;
-    units_s2 = p.nstrips * bands_s2;
-    Ks2 = min(Ks / 2, ((int)gridDim.x + units_s2 - 1) / units_s2);
-  }
-  const int bandh_s2 = (rows_all + bands_s2 - 1) / bands_s2;
   const int items_big = (K_eval - Ks) * units;
-  const int items_mid = (Ks - Ks2) * units_s;
-  const int total = items_big + items_mid + Ks2 * units_s2;
+  const int total = items_big + Ks * units_s;
+  // streamed epilogue (p.epi): output segments are the tail bands (the main
+  // bands without a tail); CTA 0 publishes the schedule, every item bumps the
+  // counters of the segments it covers once its reductions have landed
+  // (segment bookkeeping lives in shared memory: no registers held across
+  // the sweep -- the K3 register allocation is sensitive to it)
+  __shared__ int s_seg_h, s_sg0, s_sg1;
+  const int seg_h = Ks > 0 ? bandh_s : bandh;
+  if (threadIdx.x == 0) s_seg_h = seg_h;
+  if (p.epi && blockIdx.x == 0 && threadIdx.x == 0) {
+    int* ctrl = p.counter;  // [0] queue head, [1] epilogue queue head, [2..8] schedule
+    ctrl[2] = seg_h;
+    ctrl[3] = (rows_all + seg_h - 1) / seg_h;
+    ctrl[4] = bandh;
+    ctrl[5] = bandh_s;
+    ctrl[6] = Ks;
+    ctrl[7] = K_eval;
+    __threadfence();
+    atomicExch(ctrl + 8, 1);
+  }
   const int tid = threadIdx.x;
   const float centerf = p.centred ? 0.f : (float)p.stats[3];
   const float a = p.a, b = p.b;
@@ -307,27 +336,43 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
 
   VState<R, PASSES> st;
 
-  // persistent CTA: pull (term, band, strip) items, term-major, edge strips
-  // (costlier border code) first within a band
+  // persistent CTA: pull (term, band, strip) items -- band by band (main
+  // terms, then the tail terms) so output segments complete one after
+  // another; edge strips (costlier border code) first within a band
   for (;;) {
     if (tid == 0) s_item = atomicAdd(p.counter, 1);
     __syncthreads();
     const int item = s_item;
     if (item >= total) break;
-    const int seg = item < items_big ? 0 : (item < items_big + items_mid ? 1 : 2);
-    const int i2 = seg == 0 ? item : (seg == 1 ? item - items_big : item - items_big - items_mid);
-    const int un = seg == 0 ? units : (seg == 1 ? units_s : units_s2);
-    const int kk = (seg == 0 ? 0 : (seg == 1 ? K_eval - Ks : K_eval - Ks2)) + i2 / un;
-    const int u = i2 - (i2 / un) * un;
-    const int band = u / p.nstrips;
-    const int si = u - band * p.nstrips;
+    const bool tail = item >= items_big;
+    const int i2 = tail ? item - items_big : item;
+    int kk, band, si;
+    if (tail ? SBF_TAIL_BAND_MAJOR : SBF_MAIN_BAND_MAJOR) {
+      const int per = (tail ? Ks : K_eval - Ks) * p.nstrips;
+      band = i2 / per;
+      const int r2 = i2 - band * per;
+      kk = (tail ? K_eval - Ks : 0) + r2 / p.nstrips;
+      si = r2 - (r2 / p.nstrips) * p.nstrips;
+    } else {
+      const int un = tail ? units_s : units;
+      kk = i2 / un;
+      const int u = i2 - kk * un;
+      kk += tail ? K_eval - Ks : 0;
+      band = u / p.nstrips;
+      si = u - band * p.nstrips;
+    }
     const int strip = p.nstrips < 2 ? si : (si == 0 ? 0 : (si == 1 ? p.nstrips - 1 : si - 1));
-    const int bh = seg == 0 ? bandh : (seg == 1 ? bandh_s : bandh_s2);
+    const int bh = tail ? bandh_s : bandh;
 
   const int y0 = p.out_lo + band * bh;
   const int y1 = min(p.out_hi, y0 + bh);
   const int Bn = y1 - y0;
   const int T_total = Bn + 2 * HALO;
+  if (SBF_EPI_COUNTERS && p.epi && tid == 0) {
+    const int sh = s_seg_h;
+    s_sg0 = (y0 - p.out_lo) / sh;
+    s_sg1 = (y1 - 1 - p.out_lo) / sh;
+  }
   const int xs = strip * WC - HALO;  // image column of haloed index 0
 
   // ---- border tables: index = stream/haloed position + GOFF ----
@@ -625,6 +670,13 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
       __syncthreads();
     }  // chunks
   }  // term item
+    if (SBF_EPI_COUNTERS && p.epi) {
+      // every thread's reductions are ordered before the segment counters move
+      __threadfence();
+      __syncthreads();
+      if (tid == 0)
+        for (int sg = s_sg0; sg <= s_sg1; ++sg) atomicAdd(p.seg_done + sg, 1);
+    }
   }  // work queue
 }
 
