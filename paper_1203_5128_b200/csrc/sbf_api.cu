@@ -205,7 +205,10 @@ constexpr int kEpiThreads = 64;
 constexpr int kEpiPx = 4096;  // pixels per chunk
 constexpr long long kEpiTimeout = 1ll << 33;  // cycles (~4 s): only a failed K3 gets here
 
-// <= 64 registers: two warps fit in the 4096 registers a 2-CTA K3 (240 regs) leaves
+// <= 64 registers: two warps would fit beside two K3 CTAs of <= 240 registers
+// (the r=4 kernel takes 249, and capping it costs more than co-residency
+// gains: 483 us at 248, 652 us at 240 vs 464 us), so in practice the CTAs
+// start as K3 CTAs retire and divide out the segments already complete
 __global__ void __launch_bounds__(kEpiThreads, 16) stream_epilogue_kernel(const StreamEpi e) {
   __shared__ int s_c, s_ok;
   volatile int* vc = e.ctrl;
