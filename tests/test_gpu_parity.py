@@ -309,11 +309,13 @@ def test_coarse_nlm_budgets():
         P.PatchSpec(((1, 0),), (10.0,))
 
 
-@pytest.mark.parametrize("shape,spatial,integer", [
-    ((96, 80), None, False), ((37, 130), None, True), ((9, 9), None, False),
-    ((64, 64), ("box", 3), True), ((50, 61), ("iter", 2.5, 2), False),
-    ((70, 33), ("iter", 2.5, 2), True)])
-def test_dual_form_matches_term_sweeps_and_oracle(shape, spatial, integer):
+@pytest.mark.parametrize("shape,spatial,integer,sigma_r", [
+    ((96, 80), None, False, 2000.0), ((37, 130), None, True, 2000.0), ((9, 9), None, False, 2000.0),
+    ((64, 64), ("box", 3), True, 2000.0), ((50, 61), ("iter", 2.5, 2), False, 2000.0),
+    ((70, 33), ("iter", 2.5, 2), True, 2000.0),
+    # sigma_r 800 (config 3's)
+    ((96, 80), None, True, 800.0), ((45, 77), ("iter", 2.5, 2), True, 800.0)])
+def test_dual_form_matches_term_sweeps_and_oracle(shape, spatial, integer, sigma_r):
     """HDR plans with M = 0: the dual evaluation cos(gamma s)^N over the window
     (tabulated for integer-valued images, powered otherwise) equals the K-term
     sweeps and the oracle."""
@@ -328,8 +330,8 @@ def test_dual_form_matches_term_sweeps_and_oracle(shape, spatial, integer):
         sp, osp = P.Box(spatial[1]), ("box", spatial[1])
     else:
         sp, osp = P.IteratedBox(spatial[1], spatial[2]), ("iterated", spatial[1], spatial[2])
-    params = P.FilterParams(sigma_s=3.0, sigma_r=2000.0, epsilon=0.01, spatial=sp)
-    ref = O.shiftable_bf(img, 3.0, 2000.0, 0.01, spatial=osp)
+    params = P.FilterParams(sigma_s=3.0, sigma_r=sigma_r, epsilon=0.01, spatial=sp)
+    ref = O.shiftable_bf(img, 3.0, sigma_r, 0.01, spatial=osp)
     assert ref["M"] == 0
     outs = []
     try:
