@@ -10,6 +10,7 @@ GPU as K1 (local range) -> K2 (plan on device) -> K3 (fused term kernel)
 from __future__ import annotations
 
 import functools
+import threading
 import warnings
 from dataclasses import dataclass
 from typing import NamedTuple, Optional
@@ -100,10 +101,15 @@ def shiftable_bf(img, params: FilterParams) -> ShiftableResult:
     folded frequency, then num/den with the non-positive-normaliser
     fallback (RuntimeWarning + count).
     """
+    import torch
+
+    # the zeroed meta block is queued before the input copy: off the critical path
+    dev = img.device if isinstance(img, torch.Tensor) and img.is_cuda else None
+    meta = torch.zeros(_META_BYTES, dtype=torch.uint8, device=dev or "cuda")
     s = stage(img)
     numpy_in = s.host and not s.torch_in
     out, plan, fallbacks = _filter_staged(s, params, out_f64=(numpy_in or s.dtype == _lib.SBF_F64),
-                                          to_host=s.host)
+                                          to_host=s.host, meta=meta)
     if fallbacks:
         warnings.warn(f"{fallbacks} pixel(s) had a non-positive normalizer; input values kept",
                       RuntimeWarning, stacklevel=2)
@@ -118,6 +124,22 @@ def shiftable_bf(img, params: FilterParams) -> ShiftableResult:
 _META_PLAN, _META_FB, _META_STATS, _META_BYTES = 0, 64, 128, 256
 
 
+_tls = threading.local()
+
+
+def _read_meta(meta):
+    """Copy the device meta block into a per-thread page-locked buffer and
+    wait for the stream (cheaper than a pageable .cpu() round trip)."""
+    import torch
+
+    buf = getattr(_tls, "meta", None)
+    if buf is None or buf.numel() != meta.numel():
+        buf = _tls.meta = torch.empty(meta.numel(), dtype=torch.uint8, pin_memory=True)
+    buf.copy_(meta, non_blocking=True)
+    torch.cuda.current_stream(meta.device).synchronize()
+    return buf.numpy().copy()
+
+
 @functools.lru_cache(maxsize=64)
 def _workspace_layout(H, W, dtype, sp_key, prec):
     """(total bytes, term-table offset, filter-workspace offset) of the
@@ -129,7 +151,7 @@ def _workspace_layout(H, W, dtype, sp_key, prec):
     return max(total, 256), terms_off, terms_off + ((TERMS_CAP * 32 + 255) // 256) * 256
 
 
-def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False):
+def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False, meta=None):
     """K1..K4 on a staged device image; returns (output, KernelPlan, fallbacks).
 
     One C call (sbf_shiftable_bf) launches the whole pipeline without a host
@@ -157,7 +179,8 @@ def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False
     l2e = log_2_over_eps(params.epsilon)
     total, terms_off, fws_off = _workspace_layout(
         H, W, s.dtype, (sp.mode, sp.passes, sp.r, 0, sp.alpha, sp.sigma_s), prec)
-    meta = torch.zeros(_META_BYTES, dtype=torch.uint8, device=dev)
+    if meta is None:
+        meta = torch.zeros(_META_BYTES, dtype=torch.uint8, device=dev)
     ws = torch.empty(total, dtype=torch.uint8, device=dev)
     plan_ptr = meta.data_ptr() + _META_PLAN
     fb_ptr = meta.data_ptr() + _META_FB
@@ -173,7 +196,7 @@ def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False
                                     float(params.sigma_r), float(params.epsilon), rule, l2e, prec,
                                     out.data_ptr(), out_dtype, plan_ptr, stats_ptr, fb_ptr,
                                     TERMS_CAP, ws.data_ptr(), total, stream), "shiftable_bf")
-    tail = meta.cpu().numpy()
+    tail = _read_meta(meta)
     stats_host = tail[_META_STATS:_META_STATS + 64]
     if int(stats_host.view(np.uint64)[7]) != 0:
         raise InvalidParameterError("image contains non-finite samples")
@@ -186,7 +209,7 @@ def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False
         _lib.check(lib.sbf_filter(s.tensor.data_ptr(), s.dtype, H, W, W, 0, H, 0, H, sp, plan_ptr,
                                   terms_ptr, stats_ptr, prec, out.data_ptr(), out_dtype, fb_ptr,
                                   ws.data_ptr() + fws_off, total - fws_off, stream), "filter")
-        t = meta.cpu().numpy()
+        t = _read_meta(meta)
         return (_lib.SbfPlan.from_buffer_copy(t[_META_PLAN:_META_PLAN + 64].tobytes()),
                 int(t[_META_FB:_META_FB + 8].view(np.int64)[0]))
 

@@ -86,10 +86,15 @@ def _stage_pinned(t, device=None):
     kind = _STAGE_KINDS[t.dtype]
     out_dtype = torch.float64 if kind == _lib.STAGE_F64 else torch.float32
     dev = torch.empty(tuple(t.shape), dtype=out_dtype, device=device or "cuda")
-    with torch.cuda.device(dev.device):
-        stream = torch.cuda.current_stream().cuda_stream
-        _lib.check(_lib.load().sbf_stage_h2d(t.data_ptr(), kind, t.numel(), dev.data_ptr(), stream),
-                   "stage_h2d")
+    lib = _lib.load()
+    if dev.device.index == torch.cuda.current_device():
+        rc = lib.sbf_stage_h2d(t.data_ptr(), kind, t.numel(), dev.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream)
+    else:
+        with torch.cuda.device(dev.device):
+            rc = lib.sbf_stage_h2d(t.data_ptr(), kind, t.numel(), dev.data_ptr(),
+                                   torch.cuda.current_stream().cuda_stream)
+    _lib.check(rc, "stage_h2d")
     # the read is stream-ordered; every public entry point synchronises on its
     # result before returning, so `t` outlives it
     return dev
