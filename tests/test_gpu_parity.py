@@ -366,3 +366,27 @@ def test_split_sweep_matches_strip_kernel_and_oracle(shape, sigma_s, sigma_r):
     finally:
         lib.sbf_set_split_min_radius(9)
     assert float(np.abs(outs[0] - outs[1]).max()) < 5e-3
+
+
+@pytest.mark.parametrize("mode", [0, 2])
+def test_strips_with_streamed_epilogue(mode):
+    """Strips (out_lo > 0, buffer row offsets) through K3 with the epilogue
+    streamed behind it (mode 2, forced on device outputs) or launched plainly
+    (mode 0): both equal the full-image filter."""
+    import torch
+    from paper_1203_5128_b200.dist import StripFilter, gather_strips, strip_halo, strip_plan
+    lib = _lib.load()
+    img = config_image(2, size=512)
+    params = P.FilterParams(sigma_s=5.0, sigma_r=10.0, epsilon=0.01, precision="fp32")
+    full = P.shiftable_bf(img, params)
+    t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+    strips = strip_plan(img.shape[0], 3, strip_halo(params))
+    prev = lib.sbf_set_fused_epilogue(mode)
+    try:
+        fs = [StripFilter([t[s.buf_lo:s.buf_hi]], s, img.shape[0], params) for s in strips]
+        Tg = torch.stack([f.local_T().clone() for f in fs]).max(dim=0).values
+        outs = [f.finish(Tg)[0].cpu().numpy() for f in fs]
+    finally:
+        lib.sbf_set_fused_epilogue(prev)
+    assert float(Tg[0]) == full.plan.T
+    assert_close_image(gather_strips(outs, strips), full.image, 2e-3, 2e-4)
