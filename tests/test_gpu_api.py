@@ -216,3 +216,27 @@ def test_streamed_epilogue_matches_plain(shape, dtype, ss, sr, eps):
     assert eps < 0.1 or host.fallback_pixels > 0  # the fallback branch is exercised
     ok &= np.abs(o["image"] - img) <= span
     assert float(np.abs(host.image.numpy().astype(np.float64) - o["image"])[ok].max()) <= 1e-2
+
+
+def test_pinned_hdr_input_reruns_fp64_into_host_output():
+    """A page-locked 16-bit HDR image: the guarded fp32 K3 bails out (and with
+    it the streamed epilogue), the wrapper re-runs the fp64 path straight into
+    the page-locked result; equal to the CUDA-input call and the oracle."""
+    import torch
+    from oracle import coracle as CO
+
+    rng = np.random.default_rng(11)
+    img = np.round(rng.uniform(0, 65535, (96, 130))).astype(np.uint16)
+    img[:48] //= 8
+    params = P.FilterParams(sigma_s=2.0, sigma_r=900.0, epsilon=0.01)
+    pinned = torch.from_numpy(img.astype(np.int32)).to(torch.uint16).pin_memory() \
+        if hasattr(torch, "uint16") else torch.from_numpy(img.astype(np.float32)).pin_memory()
+    host = P.shiftable_bf(pinned, params)
+    dev = P.shiftable_bf(torch.from_numpy(img.astype(np.float32)).cuda(), params)
+    assert not host.image.is_cuda
+    assert host.plan == dev.plan
+    assert float((host.image.double() - dev.image.cpu().double()).abs().max()) <= 1e-2
+    CO.build()
+    o = CO.shiftable_bf(img.astype(np.float64), 2.0, 900.0, 0.01)
+    assert (host.plan.T, host.plan.N, host.plan.M) == (o["T"], o["N"], o["M"])
+    assert float(np.abs(host.image.double().numpy() - o["image"]).max()) <= 1e-2
