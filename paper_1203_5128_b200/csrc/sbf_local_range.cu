@@ -17,6 +17,17 @@ namespace sbf {
 namespace {
 
 constexpr int kRowSeg = 1024;   // outputs per row-pass CTA
+#ifndef SBF_K1_VH_ROW
+#define SBF_K1_VH_ROW 0  // measured: the doubling row pass is faster (21.7 vs 24.0 us, config 2)
+#endif
+#ifndef SBF_K1_VH_ROWS
+#define SBF_K1_VH_ROWS 8
+#endif
+#ifndef SBF_K1_VH_COL
+#define SBF_K1_VH_COL 1
+#endif
+constexpr bool g_k1_vh_row = SBF_K1_VH_ROW;  // van Herk blocks (else the doubling ladder)
+constexpr bool g_k1_vh_col = SBF_K1_VH_COL;
 constexpr int kColTile = 32;    // columns per column-pass CTA
 constexpr int kColRows = 64;    // output rows per column-pass CTA
 constexpr int kColThreadsY = 8;
@@ -53,12 +64,19 @@ __global__ void __launch_bounds__(256) rowmax_kernel(const T* __restrict__ f, in
   const int plen = nblk * win;
   T* suf = q + plen;
   const T* row = f + y * ld;
-  // loads batched 4 deep per thread (independent, so they overlap in flight)
+  // loads batched 4 deep per thread (independent, so they overlap in flight);
+  // interior segments need no clamping
+  if (x0 - R >= 0 && x0 - R + len <= W) {
+    const T* src = row + (x0 - R);
 #pragma unroll 4
-  for (int k = threadIdx.x; k < len; k += blockDim.x) {
-    int64_t x = x0 - R + k;
-    x = x < 0 ? 0 : (x >= W ? W - 1 : x);
-    q[k] = __ldg(row + x);
+    for (int k = threadIdx.x; k < len; k += blockDim.x) q[k] = __ldg(src + k);
+  } else {
+#pragma unroll 4
+    for (int k = threadIdx.x; k < len; k += blockDim.x) {
+      int64_t x = x0 - R + k;
+      x = x < 0 ? 0 : (x >= W ? W - 1 : x);
+      q[k] = __ldg(row + x);
+    }
   }
   __syncthreads();
   // doubling: a[i] = max over [i, i + span) (every element in parallel,
@@ -67,6 +85,7 @@ __global__ void __launch_bounds__(256) rowmax_kernel(const T* __restrict__ f, in
   T* b = suf;
   int span = 1;
   while (2 * span <= win) {
+#pragma unroll 4
     for (int i = threadIdx.x; i <= len - 2 * span; i += blockDim.x) b[i] = vmax(a[i], a[i + span]);
     __syncthreads();
     T* t = a;
@@ -75,7 +94,90 @@ __global__ void __launch_bounds__(256) rowmax_kernel(const T* __restrict__ f, in
     span *= 2;
   }
   T* orow = out + y * W + x0;
+#pragma unroll 4
   for (int j = threadIdx.x; j < nout; j += blockDim.x) orow[j] = vmax(a[j], a[j + win - span]);
+}
+
+// Suffix maxima of x[0..n) (stride `st`) into h, prefix maxima in place:
+// samples are read 8 at a time ahead of the stores, so the shared-memory
+// latency is paid once per chunk, not once per sample.
+template <typename T>
+__device__ __forceinline__ void vh_scan(T* __restrict__ x, T* __restrict__ h, int n, int st) {
+  T m = x[(n - 1) * st];
+  h[(n - 1) * st] = m;
+  for (int i0 = n - 2; i0 >= 0; i0 -= 8) {
+    T v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i0 - u >= 0) v[u] = x[(i0 - u) * st];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i0 - u >= 0) {
+        m = vmax(m, v[u]);
+        h[(i0 - u) * st] = m;
+      }
+  }
+  m = x[0];
+  for (int i0 = 1; i0 < n; i0 += 8) {
+    T v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i0 + u < n) v[u] = x[(i0 + u) * st];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i0 + u < n) {
+        m = vmax(m, v[u]);
+        x[(i0 + u) * st] = m;
+      }
+  }
+}
+
+// Van Herk / Gil-Werman row pass: `rows` rows x one kRowSeg segment per CTA.
+// The replicate-padded segment is cut into blocks of win = 2R+1 samples; per
+// block one thread builds the suffix maxima (h) and, in place, the prefix
+// maxima (g); output j is max(h[j], g[j + 2R]) -- 3 comparisons per sample
+// whatever R (the doubling ladder took ~log2(win) passes of shared-memory
+// traffic per sample and was instruction-bound).  Block strides are odd
+// (win), so a warp's scan accesses are bank-conflict free.
+template <typename T>
+__global__ void __launch_bounds__(256) rowmax_vh_kernel(const T* __restrict__ f, int64_t H,
+                                                        int64_t W, int64_t ld, int R, int rows,
+                                                        T* __restrict__ out,
+                                                        double* __restrict__ stats,
+                                                        unsigned* __restrict__ done) {
+  if (stats && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) init_stats(stats, done);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int win = 2 * R + 1;
+  const int64_t x0 = (int64_t)blockIdx.x * kRowSeg;
+  const int nout = (int)smin<int64_t>(kRowSeg, W - x0);
+  const int len = nout + 2 * R;
+  const int nblk = (len + win - 1) / win;
+  const int plen = nblk * win;
+  const int64_t yb = (int64_t)blockIdx.y * rows;
+  const int nr = (int)smin<int64_t>(rows, H - yb);
+  T* q = reinterpret_cast<T*>(smem_raw);  // [rows][plen]: samples, then prefix maxima
+  T* h = q + (size_t)rows * plen;         // [rows][plen]: suffix maxima
+  // one flat loop over (row, sample), 8 loads in flight per thread; the
+  // padding past the segment is loaded too (clamped)
+#pragma unroll 8
+  for (int idx = threadIdx.x; idx < nr * plen; idx += blockDim.x) {
+    const int r = idx / plen, k = idx - r * plen;
+    int64_t x = x0 - R + k;
+    x = x < 0 ? 0 : (x >= W ? W - 1 : x);
+    q[idx] = __ldg(f + (yb + r) * ld + x);
+  }
+  __syncthreads();
+  for (int bi = threadIdx.x; bi < nr * nblk; bi += blockDim.x) {
+    const int r = bi / nblk, b = bi - r * nblk;
+    vh_scan(q + r * plen + b * win, h + r * plen + b * win, win, 1);
+  }
+  __syncthreads();
+  for (int r = 0; r < nr; ++r) {
+    T* orow = out + (yb + r) * W + x0;
+    const T* hr = h + r * plen;
+    const T* gr = q + r * plen + 2 * R;
+    for (int j = threadIdx.x; j < nout; j += blockDim.x) orow[j] = vmax(hr[j], gr[j]);
+  }
 }
 
 __device__ __forceinline__ void finalize_stats(double* stats) {
@@ -113,7 +215,9 @@ __device__ __forceinline__ double block_reduce(double v, bool is_max, double* re
 }
 
 // Column pass fused with M - f, T, min/max.  Block = 32 columns x 8 threads.
-template <typename T>
+// VH: van Herk blocks down each column (one thread per column block, see
+// rowmax_vh_kernel); otherwise the doubling ladder.
+template <typename T, bool VH>
 __global__ void __launch_bounds__(kColTile* kColThreadsY) colmax_kernel(
     const T* __restrict__ rowmax, const T* __restrict__ f, int64_t H, int64_t W, int64_t ld,
     int R, int64_t t_lo, int64_t t_hi, T* __restrict__ M_out, unsigned long long* __restrict__ red,
@@ -132,45 +236,83 @@ __global__ void __launch_bounds__(kColTile* kColThreadsY) colmax_kernel(
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int64_t x = (int64_t)blockIdx.x * kColTile + tx;
   const bool xok = x < W;
+  // the T phase's samples are requested first: their latency overlaps the
+  // tile load and the scans instead of following them
+  constexpr int FPT = kColRows / kColThreadsY;
+  T fpre[FPT];
+#pragma unroll
+  for (int i = 0; i < FPT; ++i) {
+    const int j = ty + i * kColThreadsY;
+    const int64_t y = y0 + j;
+    fpre[i] = (xok && j < nrows && y >= t_lo && y < t_hi) ? __ldg(f + y * ld + x) : T(0);
+  }
   {
     const T* colp = rowmax + (xok ? x : 0);
+    const int nload = VH ? plen : len;  // VH: the padding too (clamped)
+    const int64_t ys = y0 - R;
+    if (ys >= 0 && ys + nload <= H) {
+      // interior tile: no clamping, the row pointer advances by a constant
+      const T* pr = colp + (ys + ty) * W;
+      const int64_t step = (int64_t)kColThreadsY * W;
 #pragma unroll 8
-    for (int k = ty; k < len; k += kColThreadsY) {
-      int64_t y = y0 - R + k;
-      y = y < 0 ? 0 : (y >= H ? H - 1 : y);
-      q[k * P + tx] = xok ? __ldg(colp + y * W) : T(0);
-    }
-  }
-  __syncthreads();
-  // doubling along the column (see rowmax_kernel)
-  T* a = q;
-  T* bb = suf;
-  int span = 1;
-  while (2 * span <= win) {
-    for (int i = ty; i <= len - 2 * span; i += kColThreadsY)
-      bb[i * P + tx] = vmax(a[i * P + tx], a[(i + span) * P + tx]);
-    __syncthreads();
-    T* t = a;
-    a = bb;
-    bb = t;
-    span *= 2;
-  }
-  double tmax = 0.0, fmn = INFINITY, fmx = -INFINITY;
-  unsigned long long bad = 0;
-  if (xok) {
-    for (int j = ty; j < nrows; j += kColThreadsY) {
-      const int64_t y = y0 + j;
-      const T m = vmax(a[j * P + tx], a[(j + win - span) * P + tx]);
-      if (M_out) M_out[y * W + x] = m;
-      if (y >= t_lo && y < t_hi) {
-        const double fv = (double)f[y * ld + x];
-        bad += isfinite(fv) ? 0 : 1;       // image.py:16 (as_image finiteness)
-        tmax = fmax(tmax, (double)m - fv);  // maxfilter.py:61, float64 subtraction
-        fmn = fmin(fmn, fv);
-        fmx = fmax(fmx, fv);
+      for (int k = ty; k < nload; k += kColThreadsY, pr += step) q[k * P + tx] = xok ? __ldg(pr) : T(0);
+    } else {
+#pragma unroll 8
+      for (int k = ty; k < nload; k += kColThreadsY) {
+        int64_t y = ys + k;
+        y = y < 0 ? 0 : (y >= H ? H - 1 : y);
+        q[k * P + tx] = xok ? __ldg(colp + y * W) : T(0);
       }
     }
   }
+  __syncthreads();
+  const T* a = q;
+  int span = 1;  // outputs: max(a[j], a[j + win - span]) (doubling) / max(h[j], g[j + 2R]) (VH)
+  const T* hh = suf;
+  if (VH) {
+    // suffix maxima into suf, prefix maxima in place (q)
+    for (int b = ty; b < nblk; b += kColThreadsY) {
+      vh_scan(q + (size_t)b * win * P + tx, suf + (size_t)b * win * P + tx, win, P);
+    }
+    __syncthreads();
+  } else {
+    // doubling along the column (see rowmax_kernel)
+    T* aa = q;
+    T* bb = suf;
+    while (2 * span <= win) {
+      for (int i = ty; i <= len - 2 * span; i += kColThreadsY)
+        bb[i * P + tx] = vmax(aa[i * P + tx], aa[(i + span) * P + tx]);
+      __syncthreads();
+      T* t = aa;
+      aa = bb;
+      bb = t;
+      span *= 2;
+    }
+    a = aa;
+  }
+  // min / max / finiteness in the sample type (exact); T's subtraction in fp64
+  double tmax = 0.0;
+  T fmn_t = T(INFINITY), fmx_t = T(-INFINITY);
+  unsigned long long bad = 0;
+  if (xok) {
+#pragma unroll
+    for (int i = 0; i < FPT; ++i) {
+      const int j = ty + i * kColThreadsY;
+      if (j >= nrows) break;
+      const int64_t y = y0 + j;
+      const T m = VH ? vmax(hh[j * P + tx], q[(j + 2 * R) * P + tx])
+                     : vmax(a[j * P + tx], a[(j + win - span) * P + tx]);
+      if (M_out) M_out[y * W + x] = m;
+      if (y >= t_lo && y < t_hi) {
+        const T fv = fpre[i];
+        bad += isfinite(fv) ? 0 : 1;                 // image.py:16 (as_image finiteness)
+        tmax = fmax(tmax, (double)m - (double)fv);  // maxfilter.py:61, float64 subtraction
+        fmn_t = fmin(fmn_t, fv);
+        fmx_t = fmax(fmx_t, fv);
+      }
+    }
+  }
+  double fmn = (double)fmn_t, fmx = (double)fmx_t;
   // one combined block reduction of (T, min, max, #non-finite)
   for (int o = 16; o; o >>= 1) {
     tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
@@ -272,12 +414,24 @@ int run(const void* fv, int64_t H, int64_t W, int64_t ld, int R, int64_t t_lo, i
     {
       const int win = 2 * Rr + 1;
       const int plen = ((kRowSeg + 2 * Rr + win - 1) / win) * win;
-      const size_t smem = 2 * (size_t)plen * sizeof(T);
-      SBF_REQUIRE(smem <= 200 * 1024, SBF_ERR_UNSUPPORTED, "max-filter radius %d too large", R);
-      SBF_CHECK_CUDA(cudaFuncSetAttribute(rowmax_kernel<T>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      dim3 grid((unsigned)((W + kRowSeg - 1) / kRowSeg), (unsigned)H);
-      rowmax_kernel<T><<<grid, 256, smem, st>>>(f, W, ld, Rr, rowmax, stats, done);
+      const int64_t nseg = (W + kRowSeg - 1) / kRowSeg;
+      // rows per CTA: enough CTAs for two per SM, at most 8 (4 for fp64)
+      const int rmax = sizeof(T) == 4 ? SBF_K1_VH_ROWS : (SBF_K1_VH_ROWS + 1) / 2;
+      const int rows = (int)smax<int64_t>(1, smin<int64_t>(rmax, (H * nseg + 295) / 296));
+      const size_t smem_vh = 2 * (size_t)rows * plen * sizeof(T);
+      if (g_k1_vh_row && smem_vh <= 100 * 1024) {
+        SBF_CHECK_CUDA(cudaFuncSetAttribute(rowmax_vh_kernel<T>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_vh));
+        dim3 grid((unsigned)nseg, (unsigned)((H + rows - 1) / rows));
+        rowmax_vh_kernel<T><<<grid, 256, smem_vh, st>>>(f, H, W, ld, Rr, rows, rowmax, stats, done);
+      } else {
+        const size_t smem = 2 * (size_t)plen * sizeof(T);
+        SBF_REQUIRE(smem <= 200 * 1024, SBF_ERR_UNSUPPORTED, "max-filter radius %d too large", R);
+        SBF_CHECK_CUDA(cudaFuncSetAttribute(rowmax_kernel<T>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dim3 grid((unsigned)nseg, (unsigned)H);
+        rowmax_kernel<T><<<grid, 256, smem, st>>>(f, W, ld, Rr, rowmax, stats, done);
+      }
       SBF_CHECK_LAUNCH();
     }
     {
@@ -285,12 +439,12 @@ int run(const void* fv, int64_t H, int64_t W, int64_t ld, int R, int64_t t_lo, i
       const int plen = ((kColRows + 2 * Rc + win - 1) / win) * win;
       const size_t smem = 2 * (size_t)plen * (kColTile + 1) * sizeof(T) + 32 * sizeof(double);
       SBF_REQUIRE(smem <= 220 * 1024, SBF_ERR_UNSUPPORTED, "max-filter radius %d too large", R);
-      SBF_CHECK_CUDA(cudaFuncSetAttribute(colmax_kernel<T>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       dim3 grid((unsigned)((W + kColTile - 1) / kColTile), (unsigned)((H + kColRows - 1) / kColRows));
       dim3 block(kColTile, kColThreadsY);
-      colmax_kernel<T><<<grid, block, smem, st>>>(rowmax, f, H, W, ld, Rc, t_lo, t_hi,
-                                                  static_cast<T*>(M_out), red, done);
+      auto kern = g_k1_vh_col ? colmax_kernel<T, true> : colmax_kernel<T, false>;
+      SBF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<grid, block, smem, st>>>(rowmax, f, H, W, ld, Rc, t_lo, t_hi, static_cast<T*>(M_out),
+                                      red, done);
       SBF_CHECK_LAUNCH();
     }
     return SBF_OK;  // colmax's last CTA wrote the final statistics
