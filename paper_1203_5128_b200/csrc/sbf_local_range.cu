@@ -32,8 +32,9 @@ constexpr int kColTile = 32;    // columns per column-pass CTA
 constexpr int kColRows = 64;    // output rows per column-pass CTA
 constexpr int kColThreadsY = 8;
 
-template <typename T>
-__device__ __forceinline__ T vmax(T a, T b) { return a > b ? a : b; }
+// one FMNMX / DMNMX (the inputs are finite: non-finite images are rejected)
+__device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ double vmax(double a, double b) { return fmax(a, b); }
 
 // Row pass: out[y, x] = max f[y, clamp(x-R .. x+R)]
 __device__ __forceinline__ void init_stats(double* stats, unsigned* done) {
