@@ -153,6 +153,9 @@ __device__ __forceinline__ void static_for(F&& f) {
 // normalisation factor cnt_int / cnt(pos) on an axis of length n (0 outside)
 __device__ __forceinline__ float gfactor(int64_t pos, int64_t n, int r, float alpha) {
   if (pos < 0 || pos >= n) return 0.f;
+  // interior: cnt == cint (the fp64 ratio is 1 to within an ulp, 1.0f after
+  // rounding) -- skip the division for the bulk of the table
+  if (pos - r - 1 >= 0 && pos + r + 1 <= n - 1) return 1.f;
   const int64_t lo = pos - r < 0 ? 0 : pos - r;
   const int64_t hi = pos + r > n - 1 ? n - 1 : pos + r;
   double cnt = (double)(hi - lo + 1);
