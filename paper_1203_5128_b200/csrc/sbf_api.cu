@@ -428,6 +428,17 @@ static int launch_split_path(const FilterLaunch& a, const SplitEntry& se, int r,
   return launch_epilogue<float>(a, reinterpret_cast<const float*>(p.nd), 1, rows_out * a.W);
 }
 
+size_t k3_zero_bytes(const FilterLaunch& a) {
+  int r, passes;
+  double alpha;
+  if (!spatial_coeffs(a.sp, &r, &passes, &alpha)) return 0;
+  if (a.precision != SBF_PREC_FP32 && a.precision != SBF_PREC_AUTO) return 0;
+  if (!find_entry(a.sp, SBF_PREC_FP32) || find_split(a.sp, SBF_PREC_FP32)) return 0;
+  if (g_stage_mask != 3) return 0;
+  const int64_t rows_out = a.out_hi - a.out_lo;
+  return align_up((size_t)(rows_out * a.W) * 8) + terms_ctrl_bytes(rows_out);
+}
+
 int launch_filter(const FilterLaunch& a) {
   int r, passes;
   double alpha;
@@ -547,7 +558,7 @@ int launch_filter(const FilterLaunch& a) {
   }
   p.epi = (g_stage_mask & 3) == 3 && (g_fused_epi == 2 || out_host);
   p.seg_done = ctrl + 16;
-  if (g_stage_mask & 1) {
+  if ((g_stage_mask & 1) && !a.nd_zeroed) {
     SBF_CHECK_CUDA(cudaMemsetAsync(a.ws, 0, nd_bytes, a.stream));
   }
   if (g_stage_mask & 1) {
@@ -798,15 +809,55 @@ int sbf_shiftable_bf(const void* f, int dtype, int64_t H, int64_t W, const sbf_s
   sbf_term* terms = reinterpret_cast<sbf_term*>(w + lr);
   char* fws = w + lr + align_up((size_t)terms_cap * sizeof(sbf_term));
   const bool use_fixed = fixed_T >= 0.0;
-  int rc = sbf_local_range(f, dtype, H, W, W, use_fixed ? 0 : R, 0, H, nullptr, stats_dev, w, lr,
-                           stream);
-  if (rc != SBF_OK) return rc;
-  rc = sbf_plan_device(stats_dev, use_fixed ? 1 : 0, fixed_T, sigma_r, epsilon, rule,
-                       log_2_over_eps, plan_dev, terms, terms_cap, stream);
-  if (rc != SBF_OK) return rc;
-  return sbf_filter(f, dtype, H, W, W, 0, H, 0, H, sp, plan_dev, terms, stats_dev, precision, out,
-                    out_dtype, fallback_dev, fws, ws_bytes - lr -
-                    align_up((size_t)terms_cap * sizeof(sbf_term)), stream);
+  int rc;
+  sbf::FilterLaunch a;
+  a.f = f;
+  a.dtype = dtype;
+  a.H = H;
+  a.W = W;
+  a.ld = W;
+  a.row0 = 0;
+  a.img_H = H;
+  a.out_lo = 0;
+  a.out_hi = H;
+  a.sp = *sp;
+  a.plan = plan_dev;
+  a.terms = terms;
+  a.stats = stats_dev;
+  a.precision = precision;
+  a.out = out;
+  a.out_dtype = out_dtype;
+  a.fallback = fallback_dev;
+  a.ws = fws;
+  a.ws_bytes = ws_bytes - lr - align_up((size_t)terms_cap * sizeof(sbf_term));
+  a.stream = as_stream(stream);
+  if (!use_fixed && R > 0) {
+    // K2 runs in K1's last CTA and K1 clears the K3 accumulator: two
+    // launches fewer
+    sbf::PlanArgs pa;
+    pa.on = 1;
+    pa.zero_bytes = sbf::k3_zero_bytes(a);
+    pa.zero = fws;
+    a.nd_zeroed = pa.zero_bytes > 0;
+    pa.rule = rule;
+    pa.cap = terms_cap;
+    pa.sigma_r = sigma_r;
+    pa.eps = epsilon;
+    pa.log_2_over_eps = log_2_over_eps;
+    pa.plan = plan_dev;
+    pa.terms = terms;
+    rc = sbf::launch_local_range(f, dtype, H, W, W, R, 0, H, nullptr, stats_dev, w, lr,
+                                 static_cast<cudaStream_t>(stream), &pa);
+    if (rc != SBF_OK) return rc;
+  } else {
+    rc = sbf_local_range(f, dtype, H, W, W, use_fixed ? 0 : R, 0, H, nullptr, stats_dev, w, lr,
+                         stream);
+    if (rc != SBF_OK) return rc;
+    rc = sbf_plan_device(stats_dev, use_fixed ? 1 : 0, fixed_T, sigma_r, epsilon, rule,
+                         log_2_over_eps, plan_dev, terms, terms_cap, stream);
+    if (rc != SBF_OK) return rc;
+  }
+  return sbf::launch_filter(a);
 }
 
 int sbf_shiftable_bf_host(const double* f_host, int64_t H, int64_t W, const sbf_spatial* sp,

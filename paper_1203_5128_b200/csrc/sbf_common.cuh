@@ -74,10 +74,22 @@ struct TermGeom {
   size_t smem;
 };
 
+// K2 fused into K1's last CTA (whole-pipeline entry): the plan arguments
+struct PlanArgs {
+  int on;
+  int rule;
+  int cap;
+  double sigma_r, eps, log_2_over_eps;
+  sbf_plan* plan;
+  sbf_term* terms;
+  void* zero;         // K3 accumulator + control block cleared by K1 (no memset launch)
+  size_t zero_bytes;  // multiple of 16
+};
+
 // Forward declarations of internal launchers (implemented in separate TUs).
 int launch_local_range(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int R,
                        int64_t t_lo, int64_t t_hi, void* M_out, double* stats, void* ws,
-                       size_t ws_bytes, cudaStream_t st);
+                       size_t ws_bytes, cudaStream_t st, const PlanArgs* plan = nullptr);
 size_t local_range_ws(int64_t H, int64_t W, int dtype);
 
 int launch_plan(const double* T_dev, int use_fixed, double fixed_T, double sigma_r, double eps,
@@ -114,9 +126,12 @@ struct FilterLaunch {
   void* ws;
   size_t ws_bytes;
   cudaStream_t stream;
+  int nd_zeroed = 0;  // the K3 accumulator in ws is already zero (cleared by K1)
 };
 
 int launch_filter(const FilterLaunch& a);
+// bytes of ws the K3 path clears before its launch (0: another path runs)
+size_t k3_zero_bytes(const FilterLaunch& a);
 size_t filter_ws(int64_t H, int64_t W, int64_t rows_out, int dtype, const sbf_spatial* sp,
                  int precision);
 

@@ -11,7 +11,10 @@
 // HBM-bound: f is read twice (row pass, column pass) and the row maxima
 // once (written + read); T, min f and max f are reduced on chip and folded
 // into three 64-bit atomics per CTA.
+#include <cstring>
+
 #include "sbf_common.cuh"
+#include "sbf_plan_warp.cuh"
 
 namespace sbf {
 namespace {
@@ -222,7 +225,7 @@ template <typename T, bool VH>
 __global__ void __launch_bounds__(kColTile* kColThreadsY) colmax_kernel(
     const T* __restrict__ rowmax, const T* __restrict__ f, int64_t H, int64_t W, int64_t ld,
     int R, int64_t t_lo, int64_t t_hi, T* __restrict__ M_out, unsigned long long* __restrict__ red,
-    unsigned* __restrict__ done) {
+    unsigned* __restrict__ done, const PlanArgs pa) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int win = 2 * R + 1;
   const int64_t y0 = (int64_t)blockIdx.y * kColRows;
@@ -237,6 +240,16 @@ __global__ void __launch_bounds__(kColTile* kColThreadsY) colmax_kernel(
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int64_t x = (int64_t)blockIdx.x * kColTile + tx;
   const bool xok = x < W;
+  // fused pipeline: clear the K3 accumulator (its memset launch saved)
+  if (pa.zero_bytes) {
+    const int64_t n16 = (int64_t)(pa.zero_bytes / 16);
+    const int64_t nth = (int64_t)gridDim.x * gridDim.y * blockDim.x * blockDim.y;
+    uint4* z = static_cast<uint4*>(pa.zero);
+    for (int64_t i = ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x * blockDim.y +
+                     threadIdx.y * blockDim.x + threadIdx.x;
+         i < n16; i += nth)
+      z[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
   // the T phase's samples are requested first: their latency overlaps the
   // tile load and the scans instead of following them
   constexpr int FPT = kColRows / kColThreadsY;
@@ -322,6 +335,8 @@ __global__ void __launch_bounds__(kColTile* kColThreadsY) colmax_kernel(
     bad += __shfl_xor_sync(0xffffffffu, bad, o);
   }
   const int tid = ty * kColTile + tx, lane = tid & 31, warp = tid >> 5;
+  __shared__ int s_last;
+  __shared__ sbf_plan s_plan;
   if (lane == 0) {
     dred[4 * warp] = tmax;
     dred[4 * warp + 1] = fmn;
@@ -342,10 +357,20 @@ __global__ void __launch_bounds__(kColTile* kColThreadsY) colmax_kernel(
     if (bad) atomicAdd(&red[3], bad);
     // the last CTA folds the atomics into stats (no finalisation launch)
     __threadfence();
+    s_last = 0;
     if (atomicAdd(done, 1u) == gridDim.x * gridDim.y - 1) {
       __threadfence();
       finalize_stats(reinterpret_cast<double*>(red) - 4);
+      s_last = 1;
     }
+  }
+  if (pa.on) {
+    // ... and, in the fused pipeline, builds the plan with its first warp
+    // (K2 without a launch of its own)
+    __syncwarp();
+    if (warp == 0 && s_last)
+      plan_warp(lane == 0 ? (reinterpret_cast<double*>(red) - 4)[0] : 0.0, pa.sigma_r, pa.eps, pa.rule,
+                pa.log_2_over_eps, pa.plan, pa.terms, pa.cap, 0, 0, s_plan);
   }
 }
 
@@ -388,7 +413,11 @@ size_t local_range_ws_bytes(int64_t H, int64_t W) {
 
 template <typename T>
 int run(const void* fv, int64_t H, int64_t W, int64_t ld, int R, int64_t t_lo, int64_t t_hi,
-        void* M_out, double* stats, void* ws, size_t ws_bytes, cudaStream_t st) {
+        void* M_out, double* stats, void* ws, size_t ws_bytes, cudaStream_t st,
+        const PlanArgs* plan) {
+  PlanArgs pa;
+  memset(&pa, 0, sizeof(pa));
+  if (plan && R > 0) pa = *plan;
   const T* f = static_cast<const T*>(fv);
   unsigned long long* red = reinterpret_cast<unsigned long long*>(stats + 4);
   unsigned* done = nullptr;
@@ -445,7 +474,7 @@ int run(const void* fv, int64_t H, int64_t W, int64_t ld, int R, int64_t t_lo, i
       auto kern = g_k1_vh_col ? colmax_kernel<T, true> : colmax_kernel<T, false>;
       SBF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<grid, block, smem, st>>>(rowmax, f, H, W, ld, Rc, t_lo, t_hi, static_cast<T*>(M_out),
-                                      red, done);
+                                      red, done, pa);
       SBF_CHECK_LAUNCH();
     }
     return SBF_OK;  // colmax's last CTA wrote the final statistics
@@ -463,14 +492,19 @@ size_t local_range_ws(int64_t H, int64_t W, int dtype) {
 
 int launch_local_range(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int R,
                        int64_t t_lo, int64_t t_hi, void* M_out, double* stats, void* ws,
-                       size_t ws_bytes, cudaStream_t st) {
+                       size_t ws_bytes, cudaStream_t st, const PlanArgs* plan) {
+  // the fused plan needs the column pass (R > 0); the caller launches K2 otherwise
+  SBF_REQUIRE(!plan || (R > 0 && plan->plan && plan->terms && plan->cap > 0), SBF_ERR_INVALID,
+              "fused plan needs R > 0 and plan / term buffers");
   SBF_REQUIRE(f && stats, SBF_ERR_INVALID, "null pointer");
   SBF_REQUIRE(H >= 1 && W >= 1 && ld >= W, SBF_ERR_INVALID, "bad image shape %lld x %lld",
               (long long)H, (long long)W);
   SBF_REQUIRE(R >= 0, SBF_ERR_INVALID, "radius must be >= 0");
   SBF_REQUIRE(t_lo >= 0 && t_hi <= H && t_lo < t_hi, SBF_ERR_INVALID, "bad row range");
-  if (dtype == SBF_F32) return run<float>(f, H, W, ld, R, t_lo, t_hi, M_out, stats, ws, ws_bytes, st);
-  if (dtype == SBF_F64) return run<double>(f, H, W, ld, R, t_lo, t_hi, M_out, stats, ws, ws_bytes, st);
+  if (dtype == SBF_F32)
+    return run<float>(f, H, W, ld, R, t_lo, t_hi, M_out, stats, ws, ws_bytes, st, plan);
+  if (dtype == SBF_F64)
+    return run<double>(f, H, W, ld, R, t_lo, t_hi, M_out, stats, ws, ws_bytes, st, plan);
   set_error("unsupported dtype %d", dtype);
   return SBF_ERR_INVALID;
 }
