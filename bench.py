@@ -32,9 +32,13 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-# our kernels per filtered image: row max (+ statistics reset), column max
-# (+ statistics finalisation in its last CTA), plan, term sweep (K3), epilogue (K4)
-KERNELS_PER_IMAGE = 5
+# our kernels per filtered image (fused pipeline): row max (+ statistics
+# reset), column max (+ accumulator clear; statistics and the plan in its
+# last CTA), term sweep (K3), epilogue (K4)
+KERNELS_PER_IMAGE = 4
+# the strip path (config 5) plans all channels after the T all-reduce:
+# row max, column max, plan, K3, K4
+KERNELS_STRIP_IMAGE = 5
 METRIC = "Mpixel/s shiftable Gaussian BF at 1/2/4/8 B200; % of FP32/HBM roofline"
 UNIT = "Mpixel/s"
 OPS_PER_PX_TERM = 132   # phasor 4 + f*c,f*s 2 + 4 images x 6 line passes x 5 + acc 6
@@ -228,40 +232,30 @@ def run_ours(args, rank, world, dev):
     cap = 1 << 16
     stats = torch.empty(8, dtype=torch.float64, device=dev)
     plan = torch.empty(64, dtype=torch.uint8, device=dev)
-    terms = torch.empty(cap * 32, dtype=torch.uint8, device=dev)
     out = torch.empty((H, W), dtype=torch.float32, device=dev)
     fb = torch.zeros(1, dtype=torch.int64, device=dev)
-    lr_ws = torch.empty(max(256, lib.sbf_local_range_workspace(H, W, dt)), dtype=torch.uint8,
-                        device=dev)
-    f_ws = torch.empty(max(256, lib.sbf_filter_workspace(H, W, H, dt, sp, prec)), dtype=torch.uint8,
-                       device=dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     st = torch.cuda.current_stream()
     sptr = st.cuda_stream
     l2e = log_2_over_eps(p["epsilon"])
 
+    # one step = the fused device pipeline (sbf_shiftable_bf: K1 with the plan
+    # and the accumulator clear folded in, K3, K4, programmatic dependent
+    # launches); events 2/3 are recorded by the library around the K3 launch
+    pws = torch.empty(lib.sbf_shiftable_bf_workspace(H, W, dt, sp, prec, cap), dtype=torch.uint8,
+                      device=dev)
+
     def step(evs=None):
-        def rec(i):
-            if evs is not None:
-                evs[i].record(st)
-        rec(0)
-        _lib.check(lib.sbf_local_range(f.data_ptr(), dt, H, W, W, R, 0, H, None, stats.data_ptr(),
-                                       lr_ws.data_ptr(), lr_ws.numel(), sptr))
-        rec(1)
-        _lib.check(lib.sbf_plan_device(stats.data_ptr(), 0, 0.0, p["sigma_r"], p["epsilon"], 0,
-                                       l2e, plan.data_ptr(), terms.data_ptr(), cap, sptr))
-        rec(2)
-        lib.sbf_set_stage_mask(1)
-        _lib.check(lib.sbf_filter(f.data_ptr(), dt, H, W, W, 0, H, 0, H, sp, plan.data_ptr(),
-                                  terms.data_ptr(), stats.data_ptr(), prec, out.data_ptr(),
-                                  _lib.SBF_F32, fb.data_ptr(), f_ws.data_ptr(), f_ws.numel(), sptr))
-        rec(3)
-        lib.sbf_set_stage_mask(2)
-        _lib.check(lib.sbf_filter(f.data_ptr(), dt, H, W, W, 0, H, 0, H, sp, plan.data_ptr(),
-                                  terms.data_ptr(), stats.data_ptr(), prec, out.data_ptr(),
-                                  _lib.SBF_F32, fb.data_ptr(), f_ws.data_ptr(), f_ws.numel(), sptr))
-        lib.sbf_set_stage_mask(3)
-        rec(4)
+        if evs is not None:
+            evs[0].record(st)
+            lib.sbf_set_k3_events(evs[2].cuda_event, evs[3].cuda_event)
+        _lib.check(lib.sbf_shiftable_bf(f.data_ptr(), dt, H, W, sp, R, -1.0, p["sigma_r"],
+                                        p["epsilon"], 0, l2e, prec, out.data_ptr(), _lib.SBF_F32,
+                                        plan.data_ptr(), stats.data_ptr(), fb.data_ptr(), cap,
+                                        pws.data_ptr(), pws.numel(), sptr))
+        if evs is not None:
+            lib.sbf_set_k3_events(None, None)
+            evs[4].record(st)
 
     for _ in range(args.warmup):
         step()
@@ -276,6 +270,10 @@ def run_ours(args, rank, world, dev):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     evsets = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    for es in evsets:  # materialise the event handles handed to the library
+        for e in es:
+            e.record(st)
+    torch.cuda.synchronize()
     with ClockSampler(dev.index if dev.index is not None else 0) as clk:
         for k in range(args.steps):
             step(evsets[k])
@@ -285,7 +283,7 @@ def run_ours(args, rank, world, dev):
         torch.distributed.barrier()
     step_ms = [e[0].elapsed_time(e[4]) for e in evsets]
     k3_ms = [e[2].elapsed_time(e[3]) for e in evsets]
-    k1_ms = [e[0].elapsed_time(e[1]) for e in evsets]
+    k1_ms = [e[0].elapsed_time(e[2]) for e in evsets]  # K1 (+ fused plan / clear)
     total_ms = float(np.sum(step_ms))
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -482,7 +480,7 @@ def run_strips(args, rank, world, dev):
     if r_sp >= 9:
         per_step = sum(3 + 2 * (pl.N // 2 - pl.M + 1) + 1 for pl in plans)
     else:
-        per_step = KERNELS_PER_IMAGE * 3
+        per_step = KERNELS_STRIP_IMAGE * 3
     ops = OPS_PER_PX_TERM * size * size * sum(pl.N // 2 - pl.M + 1 for pl in plans)
     achieved = ops * args.steps / (total * 1e-3) / 1e12
     peak = 148 * 128 * 1.965e9 / 1e12 * world

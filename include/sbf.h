@@ -293,6 +293,9 @@ int sbf_filter_geometry(int64_t rows_out, int64_t W, const sbf_spatial* sp, int 
                         int* out7);
 int sbf_truncation_index_exact_bigint(int N, double epsilon, int* M);
 int sbf_set_stage_mask(int mask);
+/* This thread: record these cudaEvent_t (NULL: none) right before and after
+ * every K3 launch -- kernel-level timing inside the fused pipeline. */
+int sbf_set_k3_events(void* before, void* after);
 /* K3 path, this thread: the divide/fallback epilogue streamed behind the term
  * kernel (programmatic dependent launch; each output segment is divided out
  * -- and, for a page-locked host output, written over PCIe -- as soon as

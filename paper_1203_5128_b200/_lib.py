@@ -79,6 +79,7 @@ _SIGS = {
                                      C.POINTER(C.c_ulonglong)]),
     "sbf_divide_with_fallback": (_int, [_vp, _vp, _vp, _i64, _vp, _vp, _vp]),
     "sbf_set_stage_mask": (_int, [_int]),
+    "sbf_set_k3_events": (_int, [_vp, _vp]),
     "sbf_set_fused_epilogue": (_int, [_int]),
     "sbf_pgm_decode": (_int, [_vp, _int, _i64, _vp, _vp]),
     "sbf_pgm_encode": (_int, [_vp, _int, _i64, _int, _vp, _vp]),

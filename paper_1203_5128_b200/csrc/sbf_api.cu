@@ -160,6 +160,7 @@ __global__ void epilogue_kernel(const ACC* __restrict__ nd, int groups, int64_t 
   // both the accumulator and the output are fp32
   using MT = std::conditional_t<std::is_same<ACC, float>::value && std::is_same<OT, float>::value,
                                 float, double>;
+  pdl_wait();  // K3's accumulator (PDL launch)
   const int used = min(groups, plan->K_eval);
   const MT center = (MT)stats[3];  // fp32-rounded by K1: exact in either type
   unsigned long long bad_count = 0;
@@ -337,9 +338,9 @@ static int launch_epilogue(const FilterLaunch& a, const ACC* nd, int groups, int
   const dim3 grid((unsigned)((a.W + 255) / 256),
                   (unsigned)smin<int64_t>(rows, smax<int64_t>(1, 148 * 16 / ((a.W + 255) / 256))));
 #define SBF_EPI(FT, OT)                                                                      \
-  epilogue_kernel<ACC, FT, OT><<<grid, 256, 0, a.stream>>>(                                  \
-      nd, groups, gstride, a.plan, rows, a.W, static_cast<const FT*>(a.f), a.ld, a.out_lo, \
-      a.stats, static_cast<OT*>(a.out), a.fallback)
+  SBF_CHECK_CUDA(launch_pdl(epilogue_kernel<ACC, FT, OT>, grid, dim3(256), 0, a.stream, nd, groups, \
+                            gstride, a.plan, rows, a.W, static_cast<const FT*>(a.f), a.ld,        \
+                            a.out_lo, a.stats, static_cast<OT*>(a.out), a.fallback))
   if (a.dtype == SBF_F32 && a.out_dtype == SBF_F32) SBF_EPI(float, float);
   else if (a.dtype == SBF_F32 && a.out_dtype == SBF_F64) SBF_EPI(float, double);
   else if (a.dtype == SBF_F64 && a.out_dtype == SBF_F32) SBF_EPI(double, float);
@@ -354,6 +355,8 @@ static thread_local int g_stage_mask = 3;
 // fp64 evaluation choice: 0 = always the term sweeps, 1 = cost model, 2 = dual
 // whenever exact (M = 0)
 static thread_local int g_dual_mode = 1;
+// benchmarking: events recorded around the K3 launch (this thread)
+static thread_local cudaEvent_t g_k3_ev[2] = {nullptr, nullptr};
 // K4 streamed behind K3 (programmatic dependent launch, per-segment
 // completion counters): 1 = when the output is page-locked host memory,
 // 2 = always, 0 = never (plain epilogue launch)
@@ -562,8 +565,10 @@ int launch_filter(const FilterLaunch& a) {
     SBF_CHECK_CUDA(cudaMemsetAsync(a.ws, 0, nd_bytes, a.stream));
   }
   if (g_stage_mask & 1) {
+    if (g_k3_ev[0]) SBF_CHECK_CUDA(cudaEventRecord(g_k3_ev[0], a.stream));
     int rc = e->launch(p, a.stream);
     if (rc != SBF_OK) return rc;
+    if (g_k3_ev[1]) SBF_CHECK_CUDA(cudaEventRecord(g_k3_ev[1], a.stream));
   }
   if (!(g_stage_mask & 2)) return SBF_OK;
   if (!p.epi)
@@ -614,6 +619,12 @@ int sbf_set_fused_epilogue(int on) {
   if (on < 0 || on > 2) return -1;
   sbf::g_fused_epi = on;
   return prev;
+}
+
+int sbf_set_k3_events(void* before, void* after) {
+  sbf::g_k3_ev[0] = static_cast<cudaEvent_t>(before);
+  sbf::g_k3_ev[1] = static_cast<cudaEvent_t>(after);
+  return SBF_OK;
 }
 
 int sbf_set_stage_mask(int mask) {

@@ -86,6 +86,31 @@ struct PlanArgs {
   size_t zero_bytes;  // multiple of 16
 };
 
+// Programmatic dependent launch along the pipeline (K1 row pass -> column
+// pass -> K3 -> K4): a kernel launched with launch_pdl may be scheduled while
+// its predecessor still runs; it calls pdl_wait() before touching anything the
+// predecessor reads or writes, which returns once the predecessor grid has
+// completed and flushed (a no-op for an ordinary launch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // Forward declarations of internal launchers (implemented in separate TUs).
 int launch_local_range(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int R,
                        int64_t t_lo, int64_t t_hi, void* M_out, double* stats, void* ws,

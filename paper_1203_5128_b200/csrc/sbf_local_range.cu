@@ -54,6 +54,9 @@ __global__ void __launch_bounds__(256) rowmax_kernel(const T* __restrict__ f, in
                                                      int64_t ld, int R, T* __restrict__ out,
                                                      double* __restrict__ stats,
                                                      unsigned* __restrict__ done) {
+  // (PDL: the previous kernel on the stream may still read stats / f)
+  pdl_wait();
+  pdl_trigger();
   // the statistics accumulators are reset here (the column pass that updates
   // them runs after this kernel on the stream): one launch fewer
   if (stats && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) init_stats(stats, done);
@@ -227,6 +230,8 @@ __global__ void __launch_bounds__(kColTile* kColThreadsY) colmax_kernel(
     int R, int64_t t_lo, int64_t t_hi, T* __restrict__ M_out, unsigned long long* __restrict__ red,
     unsigned* __restrict__ done, const PlanArgs pa) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  pdl_trigger();
+  pdl_wait();  // the row pass (and the statistics reset) are complete
   const int win = 2 * R + 1;
   const int64_t y0 = (int64_t)blockIdx.y * kColRows;
   const int nrows = (int)smin<int64_t>(kColRows, H - y0);
@@ -460,7 +465,8 @@ int run(const void* fv, int64_t H, int64_t W, int64_t ld, int R, int64_t t_lo, i
         SBF_CHECK_CUDA(cudaFuncSetAttribute(rowmax_kernel<T>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         dim3 grid((unsigned)nseg, (unsigned)H);
-        rowmax_kernel<T><<<grid, 256, smem, st>>>(f, W, ld, Rr, rowmax, stats, done);
+        SBF_CHECK_CUDA(launch_pdl(rowmax_kernel<T>, grid, dim3(256), smem, st, f, W, ld, Rr, rowmax,
+                                  stats, done));
       }
       SBF_CHECK_LAUNCH();
     }
@@ -473,8 +479,8 @@ int run(const void* fv, int64_t H, int64_t W, int64_t ld, int R, int64_t t_lo, i
       dim3 block(kColTile, kColThreadsY);
       auto kern = g_k1_vh_col ? colmax_kernel<T, true> : colmax_kernel<T, false>;
       SBF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      kern<<<grid, block, smem, st>>>(rowmax, f, H, W, ld, Rc, t_lo, t_hi, static_cast<T*>(M_out),
-                                      red, done, pa);
+      SBF_CHECK_CUDA(launch_pdl(kern, grid, block, smem, st, rowmax, f, H, W, ld, Rc, t_lo, t_hi,
+                                static_cast<T*>(M_out), red, done, pa));
       SBF_CHECK_LAUNCH();
     }
     return SBF_OK;  // colmax's last CTA wrote the final statistics

@@ -277,8 +277,9 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
   // the streamed epilogue (launched programmatically dependent) may start
   // now: its CTAs take whatever SM room K3 leaves and wait for segments
 #if SBF_PDL_TRIGGER
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  pdl_trigger();
 #endif
+  pdl_wait();  // K1 / K2 results (PDL launch)
   const sbf_plan* plan = p.plan;
   if (plan->status != SBF_OK) return;
   if (p.hdr_guard && needs_hdr(p.stats)) {
@@ -702,7 +703,7 @@ int launch_terms(const TermParams& p, cudaStream_t st) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long grid = (long long)sms * C::MIN_BLOCKS;  // persistent CTAs
-  terms_kernel<R, PASSES><<<(unsigned)grid, C::THREADS, smem, st>>>(p);
+  SBF_CHECK_CUDA(launch_pdl(terms_kernel<R, PASSES>, dim3((unsigned)grid), dim3(C::THREADS), smem, st, p));
   SBF_CHECK_LAUNCH();
   return SBF_OK;
 }
