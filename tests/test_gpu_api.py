@@ -240,3 +240,51 @@ def test_pinned_hdr_input_reruns_fp64_into_host_output():
     o = CO.shiftable_bf(img.astype(np.float64), 2.0, 900.0, 0.01)
     assert (host.plan.T, host.plan.N, host.plan.M) == (o["T"], o["N"], o["M"])
     assert float(np.abs(host.image.double().numpy() - o["image"]).max()) <= 1e-2
+
+
+def test_fused_pipeline_graph_capture_replay():
+    """sbf_shiftable_bf (fused K1+K2, programmatic dependent launches, no host
+    sync on the K3 path) is capturable into a CUDA graph; replays on new input
+    data equal direct calls."""
+    import torch
+    from paper_1203_5128_b200 import _lib
+    from paper_1203_5128_b200.kernels import log_2_over_eps
+    from paper_1203_5128_b200.spatial import to_c_spatial
+
+    lib = _lib.load()
+    H, W = 300, 257
+    rng = np.random.default_rng(5)
+    imgs = [rng.uniform(0, 255, (H, W)).astype(np.float32) for _ in range(3)]
+    params = P.FilterParams(sigma_s=4.0, sigma_r=20.0, epsilon=0.01)
+    sp = to_c_spatial(params.resolved_spatial())
+    R = params.resolved_radius()
+    cap = 1 << 14
+    f = torch.from_numpy(imgs[0]).cuda()
+    out = torch.empty((H, W), dtype=torch.float32, device="cuda")
+    plan = torch.empty(64, dtype=torch.uint8, device="cuda")
+    stats = torch.empty(8, dtype=torch.float64, device="cuda")
+    fb = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ws = torch.empty(lib.sbf_shiftable_bf_workspace(H, W, 0, sp, _lib.PREC_FP32, cap),
+                     dtype=torch.uint8, device="cuda")
+
+    def call():
+        _lib.check(lib.sbf_shiftable_bf(f.data_ptr(), 0, H, W, sp, R, -1.0, 20.0, 0.01, 0,
+                                        log_2_over_eps(0.01), _lib.PREC_FP32, out.data_ptr(), 0,
+                                        plan.data_ptr(), stats.data_ptr(), fb.data_ptr(), cap,
+                                        ws.data_ptr(), ws.numel(),
+                                        torch.cuda.current_stream().cuda_stream), "pipeline")
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        call()  # warm-up (function attributes) outside the capture
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        call()
+    for img in imgs[1:]:
+        f.copy_(torch.from_numpy(img))
+        g.replay()
+        torch.cuda.synchronize()
+        ref = P.shiftable_bf(torch.from_numpy(img).cuda(), params).image
+        assert float((out - ref).abs().max()) <= 1e-3
