@@ -55,7 +55,9 @@ def _cfg_params(cfg):
 # clocks sampling (nvidia-smi during the timed region)
 # ----------------------------------------------------------------------------
 class ClockSampler:
-    """Polls nvidia-smi (one query per ~100 ms) on a thread during the timed region."""
+    """Samples SM clock and clock-event (throttle) reasons on a thread during
+    the timed region: NVML every ~1 ms when pynvml is importable (a config-2
+    timed region lasts ~10 ms), else nvidia-smi every ~100 ms."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -64,6 +66,28 @@ class ClockSampler:
         self.index = index
         self.lines = []
         self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._mx = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _poll_nvml(self):
+        nv, h = self._nv, self._h
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                flags = ["Active" if r & b else "Not Active" for b in bits]
+                self.lines.append(", ".join([str(self.index), str(sm), str(self._mx), "0", hex(r)] + flags))
+            except Exception:
+                pass
+            self._stop.wait(0.001)
 
     def _poll(self):
         while not self._stop.is_set():
@@ -77,7 +101,7 @@ class ClockSampler:
             self._stop.wait(0.1)
 
     def __enter__(self):
-        self.t = threading.Thread(target=self._poll, daemon=True)
+        self.t = threading.Thread(target=self._poll_nvml if self._nv else self._poll, daemon=True)
         self.t.start()
         return self
 
