@@ -274,12 +274,14 @@ __global__ void __launch_bounds__(TermCfg<R, PASSES>::THREADS, TermCfg<R, PASSES
   float* gh = gv + gv_len;
   float* FR = gh + HALO_W + GOFF;  // per-thread ring of prefetched f samples (L slots)
 
-  // the streamed epilogue (launched programmatically dependent) may start
-  // now: its CTAs take whatever SM room K3 leaves and wait for segments
+  // Wait for K1 / K2 (PDL launch), then let the dependent epilogue launch:
+  // its CTAs take whatever SM room K3 leaves and wait for segments.  The
+  // wait comes first because the streamed epilogue reads the control block
+  // that the fused K1 clears.
+  pdl_wait();
 #if SBF_PDL_TRIGGER
   pdl_trigger();
 #endif
-  pdl_wait();  // K1 / K2 results (PDL launch)
   const sbf_plan* plan = p.plan;
   if (plan->status != SBF_OK) return;
   if (p.hdr_guard && needs_hdr(p.stats)) {
