@@ -175,7 +175,8 @@ int sbf_filter(const void* f, int dtype, int64_t H, int64_t W, int64_t ld,
                void* stream);
 
 /* Whole pipeline (K1 -> K2 -> K3 -> K4) on device buffers; no host sync.
- * fixed_T < 0 means "compute T with window radius R". */
+ * fixed_T < 0 means "compute T with window radius R".  *fallback_dev is set
+ * to this call's fallback count (reset by the pipeline, not accumulated). */
 size_t sbf_shiftable_bf_workspace(int64_t H, int64_t W, int dtype,
                                   const sbf_spatial* sp, int precision,
                                   int terms_cap);

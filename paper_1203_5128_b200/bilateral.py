@@ -101,15 +101,10 @@ def shiftable_bf(img, params: FilterParams) -> ShiftableResult:
     folded frequency, then num/den with the non-positive-normaliser
     fallback (RuntimeWarning + count).
     """
-    import torch
-
-    # the zeroed meta block is queued before the input copy: off the critical path
-    dev = img.device if isinstance(img, torch.Tensor) and img.is_cuda else None
-    meta = torch.zeros(_META_BYTES, dtype=torch.uint8, device=dev or "cuda")
     s = stage(img)
     numpy_in = s.host and not s.torch_in
     out, plan, fallbacks = _filter_staged(s, params, out_f64=(numpy_in or s.dtype == _lib.SBF_F64),
-                                          to_host=s.host, meta=meta)
+                                          to_host=s.host)
     if fallbacks:
         warnings.warn(f"{fallbacks} pixel(s) had a non-positive normalizer; input values kept",
                       RuntimeWarning, stacklevel=2)
@@ -151,7 +146,25 @@ def _workspace_layout(H, W, dtype, sp_key, prec):
     return max(total, 256), terms_off, terms_off + ((TERMS_CAP * 32 + 255) // 256) * 256
 
 
-def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False, meta=None):
+def _scratch(dev, ws_bytes):
+    """Per-thread device scratch reused across calls (every call synchronises
+    before it returns): the meta block and a grow-only workspace."""
+    import torch
+
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    cache = getattr(_tls, "scratch", None)
+    if cache is None:
+        cache = _tls.scratch = {}
+    meta, ws = cache.get(key, (None, None))
+    if meta is None:
+        meta = torch.empty(_META_BYTES, dtype=torch.uint8, device=dev)
+    if ws is None or ws.numel() < ws_bytes:
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    cache[key] = (meta, ws)
+    return meta, ws
+
+
+def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False):
     """K1..K4 on a staged device image; returns (output, KernelPlan, fallbacks).
 
     One C call (sbf_shiftable_bf) launches the whole pipeline without a host
@@ -179,9 +192,9 @@ def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False
     l2e = log_2_over_eps(params.epsilon)
     total, terms_off, fws_off = _workspace_layout(
         H, W, s.dtype, (sp.mode, sp.passes, sp.r, 0, sp.alpha, sp.sigma_s), prec)
-    if meta is None:
-        meta = torch.zeros(_META_BYTES, dtype=torch.uint8, device=dev)
-    ws = torch.empty(total, dtype=torch.uint8, device=dev)
+    # the pipeline resets the fallback counter and writes plan and statistics:
+    # the meta block needs no clearing
+    meta, ws = _scratch(dev, total)
     plan_ptr = meta.data_ptr() + _META_PLAN
     fb_ptr = meta.data_ptr() + _META_FB
     stats_ptr = meta.data_ptr() + _META_STATS

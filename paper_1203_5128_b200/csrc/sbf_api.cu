@@ -811,7 +811,8 @@ int sbf_shiftable_bf(const void* f, int dtype, int64_t H, int64_t W, const sbf_s
                      double log_2_over_eps, int precision, void* out, int out_dtype,
                      sbf_plan* plan_dev, double* stats_dev, unsigned long long* fallback_dev,
                      int terms_cap, void* ws, size_t ws_bytes, void* stream) {
-  SBF_REQUIRE(sp && terms_cap > 0, SBF_ERR_INVALID, "bad arguments");
+  SBF_REQUIRE(sp && terms_cap > 0 && fallback_dev && plan_dev && stats_dev, SBF_ERR_INVALID,
+              "bad arguments");
   const size_t need = sbf_shiftable_bf_workspace(H, W, dtype, sp, precision, terms_cap);
   SBF_REQUIRE(ws && ws_bytes >= need, SBF_ERR_WORKSPACE, "workspace too small (%zu < %zu)",
               ws_bytes, need);
@@ -849,6 +850,7 @@ int sbf_shiftable_bf(const void* f, int dtype, int64_t H, int64_t W, const sbf_s
     pa.on = 1;
     pa.zero_bytes = sbf::k3_zero_bytes(a);
     pa.zero = fws;
+    pa.fb_reset = fallback_dev;
     a.nd_zeroed = pa.zero_bytes > 0;
     pa.rule = rule;
     pa.cap = terms_cap;
@@ -861,6 +863,7 @@ int sbf_shiftable_bf(const void* f, int dtype, int64_t H, int64_t W, const sbf_s
                                  static_cast<cudaStream_t>(stream), &pa);
     if (rc != SBF_OK) return rc;
   } else {
+    SBF_CHECK_CUDA(cudaMemsetAsync(fallback_dev, 0, sizeof(unsigned long long), a.stream));
     rc = sbf_local_range(f, dtype, H, W, W, use_fixed ? 0 : R, 0, H, nullptr, stats_dev, w, lr,
                          stream);
     if (rc != SBF_OK) return rc;

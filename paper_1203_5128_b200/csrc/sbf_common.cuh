@@ -84,6 +84,7 @@ struct PlanArgs {
   sbf_term* terms;
   void* zero;         // K3 accumulator + control block cleared by K1 (no memset launch)
   size_t zero_bytes;  // multiple of 16
+  unsigned long long* fb_reset;  // fallback counter reset by K1 (nullable)
 };
 
 // Programmatic dependent launch along the pipeline (K1 row pass -> column

@@ -245,7 +245,10 @@ __global__ void __launch_bounds__(kColTile* kColThreadsY) colmax_kernel(
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int64_t x = (int64_t)blockIdx.x * kColTile + tx;
   const bool xok = x < W;
-  // fused pipeline: clear the K3 accumulator (its memset launch saved)
+  // fused pipeline: reset the fallback counter and clear the K3 accumulator
+  // (their memset launches saved)
+  if (pa.fb_reset && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0)
+    *pa.fb_reset = 0ull;
   if (pa.zero_bytes) {
     const int64_t n16 = (int64_t)(pa.zero_bytes / 16);
     const int64_t nth = (int64_t)gridDim.x * gridDim.y * blockDim.x * blockDim.y;

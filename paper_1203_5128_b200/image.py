@@ -9,6 +9,7 @@ the max filter / T must stay bit-exact, so float64 data is never rounded.
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -16,6 +17,7 @@ import numpy as np
 from . import _lib
 from .errors import InvalidParameterError
 
+_tls = threading.local()
 _F32_EXACT = (np.float32, np.uint8, np.int8, np.uint16, np.int16, np.bool_)
 
 
@@ -85,7 +87,17 @@ def _stage_pinned(t, device=None):
 
     kind = _STAGE_KINDS[t.dtype]
     out_dtype = torch.float64 if kind == _lib.STAGE_F64 else torch.float32
-    dev = torch.empty(tuple(t.shape), dtype=out_dtype, device=device or "cuda")
+    # the staged copy lives only inside one (synchronising) call: reuse a
+    # per-thread buffer
+    key = (str(device or "cuda"), out_dtype, tuple(t.shape))
+    cache = getattr(_tls, "stage", None)
+    if cache is None:
+        cache = _tls.stage = {}
+    dev = cache.get(key)
+    if dev is None:
+        if len(cache) > 8:
+            cache.clear()
+        dev = cache[key] = torch.empty(tuple(t.shape), dtype=out_dtype, device=device or "cuda")
     lib = _lib.load()
     if dev.device.index == torch.cuda.current_device():
         rc = lib.sbf_stage_h2d(t.data_ptr(), kind, t.numel(), dev.data_ptr(),
