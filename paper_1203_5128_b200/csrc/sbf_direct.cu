@@ -60,42 +60,67 @@ __global__ void __launch_bounds__(256) direct_kernel_f64(const FT* __restrict__ 
   out[y * p.W + x] = (OT)(den > 0.0 ? num / den : c);
 }
 
+// RPT output rows per thread: every loaded neighbour serves RPT outputs (row
+// s of the window serves output k at dy = s - k), 2 RPT independent
+// accumulation chains; exp2 by MUFU.EX2 (ex2.approx.ftz).
+#ifndef SBF_DIRECT_ROWS
+#define SBF_DIRECT_ROWS 4
+#endif
+constexpr int kDirectRows = SBF_DIRECT_ROWS;
+
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 template <typename FT, typename OT>
 __global__ void __launch_bounds__(256) direct_kernel(const FT* __restrict__ f, OT* __restrict__ out,
                                                      const __grid_constant__ DirectParams p) {
+  constexpr int RPT = kDirectRows;
+  __shared__ float lt[2 * kDirectMaxR + 1];
+  for (int k = threadIdx.y * blockDim.x + threadIdx.x; k < 2 * p.R + 1; k += blockDim.x * blockDim.y)
+    lt[k] = p.ltap[k];
+  __syncthreads();
   const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t y0 = ((int64_t)blockIdx.y * blockDim.y + threadIdx.y) * 2;
+  const int64_t y0 = ((int64_t)blockIdx.y * blockDim.y + threadIdx.y) * RPT;
   if (x >= p.W || y0 >= p.H) return;
-  const bool two = y0 + 1 < p.H;
+  const int nr = (int)smin<int64_t>(RPT, p.H - y0);
   const int R = p.R;
-  const float c0 = (float)f[y0 * p.ld + x];
-  const float c1 = two ? (float)f[(y0 + 1) * p.ld + x] : c0;
+  float c[RPT], n[RPT], d[RPT];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    c[k] = k < nr ? (float)f[(y0 + k) * p.ld + x] : 0.f;
+    n[k] = 0.f;
+    d[k] = 0.f;
+  }
   const int dx_lo = (int)smax<int64_t>(-R, -x), dx_hi = (int)smin<int64_t>(R, p.W - 1 - x);
-  float n0 = 0.f, d0 = 0.f, n1 = 0.f, d1 = 0.f;
-  // rows y0 + dy for dy in [-R, R + 1]: row s serves output 0 at dy = s and
-  // output 1 at dy = s - 1
-  const int s_lo = (int)smax<int64_t>(-R, -y0), s_hi = (int)smin<int64_t>(R + 1, p.H - 1 - y0);
+  // rows y0 + s for s in [-R, R + RPT - 1]
+  const int s_lo = (int)smax<int64_t>(-R, -y0), s_hi = (int)smin<int64_t>(R + nr - 1, p.H - 1 - y0);
   for (int s = s_lo; s <= s_hi; ++s) {
     const FT* row = f + (y0 + s) * p.ld + x;
-    const bool use0 = s <= R;
-    const bool use1 = two && s - 1 >= -R;
-    const float ly0 = use0 ? p.ltap[s + R] : -INFINITY;
-    const float ly1 = use1 ? p.ltap[s - 1 + R] : -INFINITY;
-#pragma unroll 4
+    float ly[RPT];
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      const int dy = s - k;
+      ly[k] = (k < nr && dy >= -R && dy <= R) ? lt[dy + R] : -INFINITY;
+    }
+#pragma unroll 2
     for (int dx = dx_lo; dx <= dx_hi; ++dx) {
       const float v = (float)row[dx];
-      const float lx = p.ltap[dx + R];
-      const float e0 = v - c0, e1 = v - c1;
-      const float w0 = exp2f(fmaf(e0 * e0, p.c, ly0 + lx));
-      const float w1 = exp2f(fmaf(e1 * e1, p.c, ly1 + lx));
-      n0 = fmaf(w0, v, n0);
-      d0 += w0;
-      n1 = fmaf(w1, v, n1);
-      d1 += w1;
+      const float lx = lt[dx + R];
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        const float e = v - c[k];
+        const float w = fast_exp2(fmaf(e * e, p.c, ly[k] + lx));
+        n[k] = fmaf(w, v, n[k]);
+        d[k] += w;
+      }
     }
   }
-  out[y0 * p.W + x] = (OT)(d0 > 0.f ? n0 / d0 : c0);
-  if (two) out[(y0 + 1) * p.W + x] = (OT)(d1 > 0.f ? n1 / d1 : c1);
+#pragma unroll
+  for (int k = 0; k < RPT; ++k)
+    if (k < nr) out[(y0 + k) * p.W + x] = (OT)(d[k] > 0.f ? n[k] / d[k] : c[k]);
 }
 
 // truncated raised-cosine expansion as the range kernel (reference
@@ -149,7 +174,7 @@ int launch_direct(const void* f, void* out, const DirectParams& p, int f64math, 
     direct_kernel_f64<FT, OT><<<grid, block, 0, st>>>(static_cast<const FT*>(f),
                                                       static_cast<OT*>(out), p);
   } else {
-    dim3 grid((unsigned)((p.W + 31) / 32), (unsigned)((p.H + 15) / 16));
+    dim3 grid((unsigned)((p.W + 31) / 32), (unsigned)((p.H + 8 * kDirectRows - 1) / (8 * kDirectRows)));
     direct_kernel<FT, OT><<<grid, block, 0, st>>>(static_cast<const FT*>(f), static_cast<OT*>(out),
                                                   p);
   }
