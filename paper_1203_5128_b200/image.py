@@ -89,7 +89,9 @@ def _stage_pinned(t, device=None):
     out_dtype = torch.float64 if kind == _lib.STAGE_F64 else torch.float32
     # the staged copy lives only inside one (synchronising) call: reuse a
     # per-thread buffer
-    key = (str(device or "cuda"), out_dtype, tuple(t.shape))
+    d = torch.device(device or "cuda")
+    d = torch.device("cuda", d.index if d.index is not None else torch.cuda.current_device())
+    key = (d.index, out_dtype, tuple(t.shape))
     cache = getattr(_tls, "stage", None)
     if cache is None:
         cache = _tls.stage = {}
@@ -97,7 +99,7 @@ def _stage_pinned(t, device=None):
     if dev is None:
         if len(cache) > 8:
             cache.clear()
-        dev = cache[key] = torch.empty(tuple(t.shape), dtype=out_dtype, device=device or "cuda")
+        dev = cache[key] = torch.empty(tuple(t.shape), dtype=out_dtype, device=d)
     lib = _lib.load()
     if dev.device.index == torch.cuda.current_device():
         rc = lib.sbf_stage_h2d(t.data_ptr(), kind, t.numel(), dev.data_ptr(),
