@@ -204,7 +204,7 @@ struct StreamEpi {
 
 constexpr int kEpiThreads = 64;
 constexpr int kEpiPx = 4096;  // pixels per chunk
-constexpr long long kEpiTimeout = 1ll << 33;  // cycles (~4 s): only a failed K3 gets here
+constexpr long long kEpiTimeout = 1ll << 36;  // cycles (~35 s): a safety net, only a failed K3 gets here
 
 // <= 64 registers: two warps would fit beside two K3 CTAs of <= 240 registers
 // (the r=4 kernel takes 249, and capping it costs more than co-residency
