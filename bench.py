@@ -421,7 +421,6 @@ def run_batch(args, rank, world, dev):
             stats=torch.empty(8, dtype=torch.float64, device=dev),
             plan=torch.empty(64, dtype=torch.uint8, device=dev),
             fb=torch.zeros(1, dtype=torch.int64, device=dev)))
-    plan = lanes[0]["plan"]
     outs = [torch.empty((H, W), dtype=torch.float32, device=dev) for _ in mine]
 
     def step():
