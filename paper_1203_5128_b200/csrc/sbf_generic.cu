@@ -12,6 +12,10 @@
 
 #include "sbf_common.cuh"
 #include "sbf_generic.h"
+
+#ifndef SBF_COLPASS_SEG
+#define SBF_COLPASS_SEG 128  // samples per column segment (NLM config 2: 256 -> 5.9 ms, 128 -> 3.3, 64 -> 3.6 in colpass)
+#endif
 #include "sbf_generic_fused.cuh"
 
 namespace sbf {
@@ -208,7 +212,7 @@ int PlaneSmoother::run(double* planes, double* tmp, cudaStream_t st, int nplanes
   if (fused) {
     // input: tmp [pl][W][H] (rows as columns); output planes [pl][H][W]
     const dim3 tgridT((unsigned)((H + 31) / 32), (unsigned)((W + 31) / 32), (unsigned)nplanes);
-    const int64_t seg = 256;
+    const int64_t seg = SBF_COLPASS_SEG;
     fe->launch(tmp, planes, nplanes, W, H, seg, gx, 0, W, ca, cb, st);                // row passes
     transpose_planes<<<tgridT, tb, 0, st>>>(planes, tmp, W, H);                       // -> [pl][H][W]
     fe->launch(tmp, planes, nplanes, H, W, seg, gy, row0, img_H, ca, cb, st);         // column passes
