@@ -491,7 +491,7 @@ def run_strips(args, rank, world, dev):
         full = config_image(5, c, size=size)
         bufs.append(torch.from_numpy(np.ascontiguousarray(full[s.buf_lo:s.buf_hi])).to(dev))
         del full
-    sf = StripFilter(bufs, s, size, params)
+    sf = StripFilter(bufs, s, size, params, overlap=args.lanes > 1)
     st = torch.cuda.current_stream()
     for _ in range(args.warmup):
         sf.run()
@@ -549,7 +549,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--images", type=int, default=64, help="config 4 batch size")
     ap.add_argument("--lanes", type=int, default=3,
-                    help="config 4: streams the images alternate on (1: 6043, 2: 6118, 3: 6170, 6: 6078 Mpix/s)")
+                    help="config 4: streams the images alternate on (1: 6043, 2: 6118, 3: 6170, 6: 6078 Mpix/s); config 5: > 1 runs each channel on its own stream")
     ap.add_argument("--size", type=int, default=None, help="config 5 side (default 16384)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

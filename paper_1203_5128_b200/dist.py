@@ -95,7 +95,8 @@ class StripFilter:
     """
 
     def __init__(self, bufs, strip: Strip, img_H: int, params: FilterParams,
-                 reduce_max: Optional[Callable] = None, precision: str = "fp32"):
+                 reduce_max: Optional[Callable] = None, precision: str = "fp32",
+                 overlap: bool = False):
         import torch
         self.lib = _lib.load()
         self.bufs = [b.contiguous() for b in bufs]
@@ -123,6 +124,13 @@ class StripFilter:
         fw = max(self.lib.sbf_filter_workspace(self.H, self.W, rows_out, d, self.sp, self.prec)
                  for d in self.dt)
         self.ws = torch.empty(max(lr, fw, 256), dtype=torch.uint8, device=self.dev)
+        # overlap: each channel's K2/K3/K4 on its own stream and workspace, so
+        # one channel's kernels fill the SMs another's launch tails leave idle
+        self.overlap = bool(overlap) and C > 1
+        if self.overlap:
+            self.side = [torch.cuda.Stream(device=self.dev) for _ in range(C)]
+            self.side_ws = [self.ws] + [torch.empty(max(fw, 256), dtype=torch.uint8, device=self.dev)
+                                        for _ in range(C - 1)]
 
     def _stream(self, stream_ptr):
         import torch
@@ -158,17 +166,31 @@ class StripFilter:
         if T_global is not None:
             self.T.copy_(T_global)
         self.fb.zero_()
+        if self.overlap:
+            import torch
+            main = torch.cuda.ExternalStream(st, device=self.dev)
+            ev = torch.cuda.Event()
+            ev.record(main)
         for c, b in enumerate(self.bufs):
+            cst, ws = st, self.ws
+            if self.overlap:
+                self.side[c].wait_event(ev)
+                cst, ws = self.side[c].cuda_stream, self.side_ws[c]
             _lib.check(lib.sbf_plan_device(
                 self.T[c:c + 1].data_ptr(), 1 if use_fixed else 0,
                 float(p.fixed_T) if use_fixed else 0.0, float(p.sigma_r), float(p.epsilon),
                 _lib.RULES[p.truncation], log_2_over_eps(p.epsilon), self.plans[c].data_ptr(),
-                self.terms[c].data_ptr(), TERMS_CAP, st), "plan")
+                self.terms[c].data_ptr(), TERMS_CAP, cst), "plan")
             _lib.check(lib.sbf_filter(
                 b.data_ptr(), self.dt[c], self.H, self.W, self.W, s.buf_lo, self.img_H, lo, hi,
                 self.sp, self.plans[c].data_ptr(), self.terms[c].data_ptr(),
                 self.stats[c].data_ptr(), self.prec, self.out[c].data_ptr(), self.dt[c],
-                self.fb[c:c + 1].data_ptr(), self.ws.data_ptr(), self.ws.numel(), st), "filter")
+                self.fb[c:c + 1].data_ptr(), ws.data_ptr(), ws.numel(), cst), "filter")
+        if self.overlap:
+            for c in range(len(self.bufs)):
+                e = torch.cuda.Event()
+                e.record(self.side[c])
+                main.wait_event(e)
         return self.out
 
     def plans_host(self):

@@ -162,25 +162,30 @@ def test_divide_with_fallback_kernel():
     np.testing.assert_array_equal(out.cpu().numpy(), [0.5, 20.0, 30.0, 1.0, 50.0])
 
 
-def test_strip_filter_emulated_ranks_match_full_image():
+@pytest.mark.parametrize("overlap", [False, True])
+def test_strip_filter_emulated_ranks_match_full_image(overlap):
     """Row strips + halo + global-T max (the config-5 data path) on one GPU,
-    ranks run one after another (no inter-rank waits), equal the full image."""
+    ranks run one after another (no inter-rank waits), equal the full image;
+    `overlap` runs each channel's K2/K3/K4 on its own stream."""
     import torch
     from paper_1203_5128_b200.dist import StripFilter, gather_strips, strip_halo, strip_plan
-    img = config_image(5, 1, size=384)
+    imgs = [config_image(5, c, size=384) for c in (1, 2)]
     params = P.FilterParams(sigma_s=12.0, sigma_r=15.0, epsilon=0.01, precision="fp32")
-    full = P.shiftable_bf(img, params)
-    t = torch.from_numpy(img).cuda()
-    strips = strip_plan(img.shape[0], 3, strip_halo(params))
-    fs = [StripFilter([t[s.buf_lo:s.buf_hi]], s, img.shape[0], params) for s in strips]
+    fulls = [P.shiftable_bf(img, params) for img in imgs]
+    ts = [torch.from_numpy(img).cuda() for img in imgs]
+    H = imgs[0].shape[0]
+    strips = strip_plan(H, 3, strip_halo(params))
+    fs = [StripFilter([t[s.buf_lo:s.buf_hi] for t in ts], s, H, params, overlap=overlap)
+          for s in strips]
     Tg = torch.stack([f.local_T().clone() for f in fs]).max(dim=0).values
-    outs = [f.finish(Tg)[0].cpu().numpy() for f in fs]
+    outs = [[o.cpu().numpy() for o in f.finish(Tg)] for f in fs]
     torch.cuda.synchronize()
-    assert float(Tg[0]) == full.plan.T
-    for f in fs:
-        pl = f.plans_host()[0]
-        assert (pl.N, pl.M) == (full.plan.N, full.plan.M)
-    assert_close_image(gather_strips(outs, strips), full.image, 2e-3, 2e-4)
+    for c, full in enumerate(fulls):
+        assert float(Tg[c]) == full.plan.T
+        for f in fs:
+            pl = f.plans_host()[c]
+            assert (pl.N, pl.M) == (full.plan.N, full.plan.M)
+        assert_close_image(gather_strips([o[c] for o in outs], strips), full.image, 2e-3, 2e-4)
 
 
 def test_ambiguous_order_threshold_replanned_on_host():
