@@ -6,6 +6,9 @@
 
 #include <vector>
 
+#include <atomic>
+#include <map>
+#include <mutex>
 #include "sbf_common.cuh"
 #include "sbf_plan_logic.cuh"
 #include "sbf_generic.h"
@@ -68,17 +71,47 @@ static const TermsEntry* find_entry(const sbf_spatial& sp, int precision) {
   return nullptr;
 }
 
-static int sm_count() {
-  int dev = 0, n = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) {
+static int sm_count() { return device_sm_count(); }
+
+// ---- host-side launch helpers (cached device queries) ----
+int device_sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
     cudaGetLastError();
     return 148;
   }
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n > 0) return n;
   if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
     cudaGetLastError();
     return 148;
   }
+  cache[dev].store(n, std::memory_order_relaxed);
   return n;
+}
+
+cudaError_t ensure_dyn_smem(const void* func, size_t bytes) {
+  // cudaFuncSetAttribute costs microseconds per call; raise the limit only
+  // when a launch needs more than any earlier one on this device
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const auto key = std::make_pair(func, dev);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  }
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> g(mu);
+    size_t& v = done[key];
+    if (v < bytes) v = bytes;
+  }
+  return e;
 }
 
 // strips x bands x term-groups; groups chosen so the grid fills whole waves

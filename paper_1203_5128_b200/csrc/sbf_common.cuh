@@ -112,6 +112,11 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// Cached device queries for the launch paths (sbf_api.cu): the SM count, and
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when it must grow.
+int device_sm_count();
+cudaError_t ensure_dyn_smem(const void* func, size_t bytes);
+
 // Forward declarations of internal launchers (implemented in separate TUs).
 int launch_local_range(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int R,
                        int64_t t_lo, int64_t t_hi, void* M_out, double* stats, void* ws,

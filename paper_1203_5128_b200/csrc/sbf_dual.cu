@@ -329,8 +329,7 @@ int launch_dual_direct(const FilterLaunch& a, const sbf_plan& plan) {
   do {                                                                                           \
     const size_t smem = sizeof(double) * (size_t)(2 * S + 1) * 40 +                              \
                         sizeof(FT) * (size_t)(8 + 2 * S) * (32 + 2 * S);                         \
-    SBF_CHECK_CUDA(cudaFuncSetAttribute(dual_lut_kernel<FT, OT>,                                 \
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));\
+    SBF_CHECK_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(dual_lut_kernel<FT, OT>), smem)); \
     dual_lut_kernel<FT, OT><<<grid, tb, smem, st>>>(static_cast<const FT*>(a.f), a.H, a.W, a.ld, \
                                                a.out_lo, a.out_hi, S, Wr, Wc, lut,               \
                                                static_cast<OT*>(a.out), a.fallback); \

@@ -458,15 +458,13 @@ int run(const void* fv, int64_t H, int64_t W, int64_t ld, int R, int64_t t_lo, i
       const int rows = (int)smax<int64_t>(1, smin<int64_t>(rmax, (H * nseg + 295) / 296));
       const size_t smem_vh = 2 * (size_t)rows * plen * sizeof(T);
       if (g_k1_vh_row && smem_vh <= 100 * 1024) {
-        SBF_CHECK_CUDA(cudaFuncSetAttribute(rowmax_vh_kernel<T>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_vh));
+        SBF_CHECK_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(rowmax_vh_kernel<T>), smem_vh));
         dim3 grid((unsigned)nseg, (unsigned)((H + rows - 1) / rows));
         rowmax_vh_kernel<T><<<grid, 256, smem_vh, st>>>(f, H, W, ld, Rr, rows, rowmax, stats, done);
       } else {
         const size_t smem = 2 * (size_t)plen * sizeof(T);
         SBF_REQUIRE(smem <= 200 * 1024, SBF_ERR_UNSUPPORTED, "max-filter radius %d too large", R);
-        SBF_CHECK_CUDA(cudaFuncSetAttribute(rowmax_kernel<T>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SBF_CHECK_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(rowmax_kernel<T>), smem));
         dim3 grid((unsigned)nseg, (unsigned)H);
         SBF_CHECK_CUDA(launch_pdl(rowmax_kernel<T>, grid, dim3(256), smem, st, f, W, ld, Rr, rowmax,
                                   stats, done));
@@ -481,7 +479,7 @@ int run(const void* fv, int64_t H, int64_t W, int64_t ld, int R, int64_t t_lo, i
       dim3 grid((unsigned)((W + kColTile - 1) / kColTile), (unsigned)((H + kColRows - 1) / kColRows));
       dim3 block(kColTile, kColThreadsY);
       auto kern = g_k1_vh_col ? colmax_kernel<T, true> : colmax_kernel<T, false>;
-      SBF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      SBF_CHECK_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem));
       SBF_CHECK_CUDA(launch_pdl(kern, grid, block, smem, st, rowmax, f, H, W, ld, Rc, t_lo, t_hi,
                                 static_cast<T*>(M_out), red, done, pa));
       SBF_CHECK_LAUNCH();

@@ -371,10 +371,8 @@ template <int R, int PASSES>
 int launch_split(const SplitParams& base_p, int K_eval, cudaStream_t st) {
   using C = SplitCfg<R, PASSES>;
   const size_t svs = sv_smem_bytes<R, PASSES>(base_p.band), shs = sh_smem_bytes<R, PASSES>();
-  SBF_CHECK_CUDA(cudaFuncSetAttribute(sv_kernel<R, PASSES>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)svs));
-  SBF_CHECK_CUDA(cudaFuncSetAttribute(sh_kernel<R, PASSES>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shs));
+  SBF_CHECK_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(sv_kernel<R, PASSES>), svs));
+  SBF_CHECK_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(sh_kernel<R, PASSES>), shs));
   const int rows_out = base_p.out_hi - base_p.out_lo;
   const dim3 svg((unsigned)((base_p.W + C::SV_COLS - 1) / C::SV_COLS),
                  (unsigned)((rows_out + base_p.band - 1) / base_p.band));

@@ -699,11 +699,8 @@ template <int R, int PASSES>
 int launch_terms(const TermParams& p, cudaStream_t st) {
   using C = TermCfg<R, PASSES>;
   const size_t smem = terms_smem_bytes<R, PASSES>(p.band);
-  SBF_CHECK_CUDA(cudaFuncSetAttribute(terms_kernel<R, PASSES>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  SBF_CHECK_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(terms_kernel<R, PASSES>), smem));
+  const int sms = device_sm_count();
   const long long grid = (long long)sms * C::MIN_BLOCKS;  // persistent CTAs
   SBF_CHECK_CUDA(launch_pdl(terms_kernel<R, PASSES>, dim3((unsigned)grid), dim3(C::THREADS), smem, st, p));
   SBF_CHECK_LAUNCH();
