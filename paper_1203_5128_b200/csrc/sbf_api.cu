@@ -91,6 +91,24 @@ int device_sm_count() {
   return n;
 }
 
+void retain_default_pool() {
+  static std::atomic<unsigned long long> done{0};  // bit per device
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    cudaGetLastError();
+    return;
+  }
+  const unsigned long long bit = 1ull << dev;
+  if (done.load(std::memory_order_relaxed) & bit) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+  done.fetch_or(bit, std::memory_order_relaxed);
+}
+
 cudaError_t ensure_dyn_smem(const void* func, size_t bytes) {
   // cudaFuncSetAttribute costs microseconds per call; raise the limit only
   // when a launch needs more than any earlier one on this device

@@ -129,12 +129,21 @@ int launch_plan(const double* T_dev, int use_fixed, double fixed_T, double sigma
 
 // Stream-ordered device scratch that is released on every exit path
 // (cudaFreeAsync on the owning stream when it goes out of scope).
+// The device's default memory pool keeps freed blocks (release threshold
+// raised once per device): with the default threshold of 0 every
+// synchronisation handed the scratch back to the driver and the next call
+// re-mapped it (milliseconds of variance on the fp64 / dual paths).
+void retain_default_pool();
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   cudaStream_t st;
   explicit DevBuf(cudaStream_t s) : st(s) {}
-  cudaError_t alloc(size_t n) { return cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), st); }
+  cudaError_t alloc(size_t n) {
+    retain_default_pool();
+    return cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), st);
+  }
   ~DevBuf() {
     if (p) cudaFreeAsync(p, st);
   }
