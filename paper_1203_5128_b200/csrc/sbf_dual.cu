@@ -268,36 +268,62 @@ int launch_dual_direct(const FilterLaunch& a, const sbf_plan& plan) {
   const int passes = a.sp.mode == SBF_SPATIAL_BOX ? 1 : a.sp.passes;
   const double alpha = a.sp.mode == SBF_SPATIAL_BOX ? 0.0 : a.sp.alpha;
   const int64_t rows_out = a.out_hi - a.out_lo;
-  // the weights of sample j in output i depend on the global axis (row0, img_H)
-  // the interior row is shared by every position at least 2S from both ends
-  std::vector<double> hr((size_t)rows_out * T), hc((size_t)a.W * T);
-  std::vector<double> interior_r(T), interior_c(T);
-  const int64_t mid_r = a.img_H / 2, mid_c = a.W / 2;
-  axis_row(a.img_H, mid_r, a.sp.r, alpha, passes, S, interior_r.data());
-  axis_row(a.W, mid_c, a.sp.r, alpha, passes, S, interior_c.data());
-  for (int64_t yo = 0; yo < rows_out; ++yo) {
-    const int64_t g = a.row0 + a.out_lo + yo;
-    if (g >= 2 * S && g < a.img_H - 2 * S)
-      std::copy(interior_r.begin(), interior_r.end(), hr.begin() + yo * T);
-    else
-      axis_row(a.img_H, g, a.sp.r, alpha, passes, S, hr.data() + yo * T);
+  // the weights of sample j in output i depend on the global axis (row0, img_H);
+  // the tables of the last geometry stay on the device (per thread): building
+  // them is ~0.7 ms of host work plus two pageable copies per call
+  struct WeightTables {
+    int dev = -1, r = 0, passes = 0, S = 0;
+    int64_t rows_out = 0, g0 = 0, img_H = 0, W = 0;
+    double alpha = 0.0;
+    double *Wr = nullptr, *Wc = nullptr;
+  };
+  static thread_local WeightTables wt;
+  int dev = 0;
+  SBF_CHECK_CUDA(cudaGetDevice(&dev));
+  const int64_t g0 = a.row0 + a.out_lo;
+  if (!(wt.Wr && wt.dev == dev && wt.r == a.sp.r && wt.passes == passes && wt.S == S &&
+        wt.rows_out == rows_out && wt.g0 == g0 && wt.img_H == a.img_H && wt.W == a.W &&
+        wt.alpha == alpha)) {
+    // the interior row is shared by every position at least 2S from both ends
+    std::vector<double> hr((size_t)rows_out * T), hc((size_t)a.W * T);
+    std::vector<double> interior_r(T), interior_c(T);
+    const int64_t mid_r = a.img_H / 2, mid_c = a.W / 2;
+    axis_row(a.img_H, mid_r, a.sp.r, alpha, passes, S, interior_r.data());
+    axis_row(a.W, mid_c, a.sp.r, alpha, passes, S, interior_c.data());
+    for (int64_t yo = 0; yo < rows_out; ++yo) {
+      const int64_t g = g0 + yo;
+      if (g >= 2 * S && g < a.img_H - 2 * S)
+        std::copy(interior_r.begin(), interior_r.end(), hr.begin() + yo * T);
+      else
+        axis_row(a.img_H, g, a.sp.r, alpha, passes, S, hr.data() + yo * T);
+    }
+    for (int64_t x = 0; x < a.W; ++x) {
+      if (x >= 2 * S && x < a.W - 2 * S)
+        std::copy(interior_c.begin(), interior_c.end(), hc.begin() + x * T);
+      else
+        axis_row(a.W, x, a.sp.r, alpha, passes, S, hc.data() + x * T);
+    }
+    // replacing a geometry: cudaFree waits for any kernel still reading the
+    // previous tables
+    if (wt.Wr) cudaFree(wt.Wr);
+    if (wt.Wc) cudaFree(wt.Wc);
+    wt = WeightTables();
+    SBF_CHECK_CUDA(cudaMalloc(reinterpret_cast<void**>(&wt.Wr), sizeof(double) * hr.size()));
+    SBF_CHECK_CUDA(cudaMalloc(reinterpret_cast<void**>(&wt.Wc), sizeof(double) * hc.size()));
+    SBF_CHECK_CUDA(cudaMemcpy(wt.Wr, hr.data(), sizeof(double) * hr.size(), cudaMemcpyHostToDevice));
+    SBF_CHECK_CUDA(cudaMemcpy(wt.Wc, hc.data(), sizeof(double) * hc.size(), cudaMemcpyHostToDevice));
+    wt.dev = dev;
+    wt.r = a.sp.r;
+    wt.passes = passes;
+    wt.S = S;
+    wt.rows_out = rows_out;
+    wt.g0 = g0;
+    wt.img_H = a.img_H;
+    wt.W = a.W;
+    wt.alpha = alpha;
   }
-  for (int64_t x = 0; x < a.W; ++x) {
-    if (x >= 2 * S && x < a.W - 2 * S)
-      std::copy(interior_c.begin(), interior_c.end(), hc.begin() + x * T);
-    else
-      axis_row(a.W, x, a.sp.r, alpha, passes, S, hc.data() + x * T);
-  }
-  DevBuf<double> Wr_b(st), Wc_b(st);
   DevBuf<double2> P_b(st);
-  SBF_CHECK_CUDA(Wr_b.alloc(hr.size()));
-  SBF_CHECK_CUDA(Wc_b.alloc(hc.size()));
-  double *Wr = Wr_b.p, *Wc = Wc_b.p;
-  SBF_CHECK_CUDA(cudaMemcpyAsync(Wr, hr.data(), sizeof(double) * hr.size(),
-                                 cudaMemcpyHostToDevice, st));
-  SBF_CHECK_CUDA(cudaMemcpyAsync(Wc, hc.data(), sizeof(double) * hc.size(),
-                                 cudaMemcpyHostToDevice, st));
-  // pageable sources: the copies above are staged before cudaMemcpyAsync returns
+  const double *Wr = wt.Wr, *Wc = wt.Wc;
   const unsigned gpix = (unsigned)smin<int64_t>((a.H * a.W + 255) / 256, 148 * 16);
   const dim3 tb(32, 8), grid((unsigned)((a.W + 31) / 32), (unsigned)((rows_out + 7) / 8));
 
