@@ -13,9 +13,6 @@
 #include "sbf_common.cuh"
 #include "sbf_generic.h"
 
-#ifndef SBF_COLPASS_SEG
-#define SBF_COLPASS_SEG 128  // samples per column segment (NLM config 2: 256 -> 5.9 ms, 128 -> 3.3, 64 -> 3.6 in colpass)
-#endif
 #include "sbf_generic_fused.cuh"
 
 namespace sbf {
@@ -212,10 +209,24 @@ int PlaneSmoother::run(double* planes, double* tmp, cudaStream_t st, int nplanes
   if (fused) {
     // input: tmp [pl][W][H] (rows as columns); output planes [pl][H][W]
     const dim3 tgridT((unsigned)((H + 31) / 32), (unsigned)((W + 31) / 32), (unsigned)nplanes);
-    const int64_t seg = SBF_COLPASS_SEG;
-    fe->launch(tmp, planes, nplanes, W, H, seg, gx, 0, W, ca, cb, st);                // row passes
+    // segment length: the longest (least recomputed warm-up) that still gives
+    // two CTAs of 128 column streams per SM.  NLM config 2 (4 planes of
+    // 1024^2): 256 -> 5.9 ms of column passes, 128 -> 3.1, 96 -> 2.5,
+    // 64 -> 3.6; large images keep 256.
+    auto seg_for = [&](int64_t n_stream, int64_t n_cols) {
+      const int64_t want = (int64_t)device_sm_count() * 2 * 128;
+      int64_t seg = 64;
+      for (int64_t cand : {256, 192, 128, 96}) {
+        if ((int64_t)nplanes * n_cols * ((n_stream + cand - 1) / cand) >= want) {
+          seg = cand;
+          break;
+        }
+      }
+      return seg;
+    };
+    fe->launch(tmp, planes, nplanes, W, H, seg_for(W, H), gx, 0, W, ca, cb, st);        // row passes
     transpose_planes<<<tgridT, tb, 0, st>>>(planes, tmp, W, H);                       // -> [pl][H][W]
-    fe->launch(tmp, planes, nplanes, H, W, seg, gy, row0, img_H, ca, cb, st);         // column passes
+    fe->launch(tmp, planes, nplanes, H, W, seg_for(H, W), gy, row0, img_H, ca, cb, st);  // column passes
   } else {
     // input and output: planes [pl][H][W]
     for (int ps = 0; ps < passes; ++ps) {
