@@ -183,7 +183,7 @@ size_t filter_ws(int64_t H, int64_t W, int64_t rows_out, int dtype, const sbf_sp
   if (!e) return align_up((size_t)(rows_out * W) * 16);  // generic: one fp64 accumulator
   TermGeom g;
   choose_geometry(*e, rows_out, W, &g);
-  // accumulator + queue heads and per-segment counters of the fused epilogue
+  // accumulator + queue heads and per-segment counters of the streamed epilogue
   size_t bytes = align_up((size_t)(rows_out * W) * 8) + terms_ctrl_bytes(rows_out);
   if (dtype == SBF_F64) bytes += align_up((size_t)(H * W) * 4);
   return bytes;

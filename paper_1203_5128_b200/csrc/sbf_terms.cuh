@@ -29,7 +29,10 @@
 //  * Accumulate — (num, den) = sums of the products, added with vector
 //    red.add.v2.f32 into one zero-initialised accumulator (L2-resident).
 // Persistent CTAs (one or two per SM) pull (term, band, strip) work items
-// from an atomic counter, so border strips and short bands balance out.
+// from an atomic counter, band by band, so border strips and short bands
+// balance out; with the streamed epilogue each item also bumps the
+// completion counters of the output segments it covers.  Launched as a
+// programmatic dependent of K1 (waits, then lets its own dependent launch).
 // Intermediate images never touch HBM.
 #pragma once
 
