@@ -288,3 +288,47 @@ def test_fused_pipeline_graph_capture_replay():
         torch.cuda.synchronize()
         ref = P.shiftable_bf(torch.from_numpy(img).cuda(), params).image
         assert float((out - ref).abs().max()) <= 1e-3
+
+
+def test_k3_event_hook_brackets_the_term_kernel():
+    """sbf_set_k3_events: the library records the caller's events around each
+    K3 launch of the fused entry (kernel timing inside one C call)."""
+    import torch
+    from paper_1203_5128_b200 import _lib
+    from paper_1203_5128_b200.kernels import log_2_over_eps
+    from paper_1203_5128_b200.spatial import to_c_spatial
+
+    lib = _lib.load()
+    H, W = 256, 300
+    img = np.random.default_rng(9).uniform(0, 255, (H, W)).astype(np.float32)
+    params = P.FilterParams(sigma_s=5.0, sigma_r=10.0, epsilon=0.01)
+    sp = to_c_spatial(params.resolved_spatial())
+    cap = 1 << 14
+    f = torch.from_numpy(img).cuda()
+    out = torch.empty((H, W), dtype=torch.float32, device="cuda")
+    plan = torch.empty(64, dtype=torch.uint8, device="cuda")
+    stats = torch.empty(8, dtype=torch.float64, device="cuda")
+    fb = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ws = torch.empty(lib.sbf_shiftable_bf_workspace(H, W, 0, sp, _lib.PREC_FP32, cap),
+                     dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream()
+    e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+    for e in (e0, e1, e2, e3):
+        e.record(st)  # materialise the handles
+    torch.cuda.synchronize()
+    e0.record(st)
+    assert lib.sbf_set_k3_events(e1.cuda_event, e2.cuda_event) == 0
+    try:
+        _lib.check(lib.sbf_shiftable_bf(f.data_ptr(), 0, H, W, sp, params.resolved_radius(), -1.0,
+                                        10.0, 0.01, 0, log_2_over_eps(0.01), _lib.PREC_FP32,
+                                        out.data_ptr(), 0, plan.data_ptr(), stats.data_ptr(),
+                                        fb.data_ptr(), cap, ws.data_ptr(), ws.numel(),
+                                        st.cuda_stream), "pipeline")
+    finally:
+        lib.sbf_set_k3_events(None, None)
+    e3.record(st)
+    e3.synchronize()
+    k1, k3, k4 = e0.elapsed_time(e1), e1.elapsed_time(e2), e2.elapsed_time(e3)
+    assert k1 > 0 and k3 > 0 and k4 >= 0 and k3 > k4
+    ref = P.shiftable_bf(f, params).image
+    assert float((out - ref).abs().max()) <= 1e-3
