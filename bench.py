@@ -1,18 +1,24 @@
 """Benchmark contract for the B200 shiftable bilateral filter.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 2] [--no-cpu-baseline]
+                    [--config 4] [--no-cpu-baseline]
 
-One "step" = one pass of the hot path over one image of the workload:
-K1 local range -> K2 device plan -> K3 fused term kernel -> K4 epilogue,
-input resident in HBM, no host synchronisation inside the step.  Default
-workload: BASELINE.json configs[1] (1024x1024 float32, sigma_s=5,
-sigma_r=10, eps=0.01), seeded synthetic input.
-L2 (126 MB) is flushed between timed steps by writing a 256 MiB buffer.
-Multi-GPU (torchrun): config 2 is single-GPU by definition, so every rank
-filters its own replica (weak scaling, no collective on the data path);
-timing is max over ranks of device-event time.
-Prints exactly one JSON line on rank 0.
+Default workload: BASELINE.json configs[3], the configuration the metric
+("Mpixel/s ... at 1/2/4/8 B200") is quoted on: a batch of 64 seeded
+4096x4096 float32 images (SURVEY.md Appendix A generator), sigma_s=6,
+sigma_r=20, eps=0.01.  One step = the whole batch through the device
+pipeline (K1 local range + plan, K3 fused term sweep with the divide /
+fallback epilogue), inputs resident in HBM.  The images are sharded over
+the ranks by px*K (LPT) with no collective on the data path; each rank's
+images rotate over three CUDA streams.  Inputs (64 MiB each) exceed what
+L2 keeps across images, so no flush is needed between steps.
+
+`--config 5` runs the 3 x 16384^2 row-strip workload (global T by an NCCL
+max all-reduce); `--config 1/2/3` run single images (replicas for N>1).
+
+`--gpus N` without torchrun environment variables re-launches this script
+under `torch.distributed.run` with N ranks (one per GPU, NCCL).  Timing is
+device-event time, max over ranks.  Rank 0 prints one JSON line.
 """
 
 from __future__ import annotations
@@ -22,6 +28,7 @@ import gc
 import json
 import multiprocessing as mp
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -33,22 +40,61 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 # our kernels per filtered image (fused pipeline): row max (+ statistics
-# reset), column max (+ accumulator clear; statistics and the plan in its
-# last CTA), term sweep (K3), epilogue (K4)
+# reset), column max (+ accumulator clear, plan in its last CTA), K3 term
+# sweep, K4 epilogue
 KERNELS_PER_IMAGE = 4
-# the strip path (config 5) plans all channels after the T all-reduce:
-# row max, column max, plan, K3, K4
-KERNELS_STRIP_IMAGE = 5
 METRIC = "Mpixel/s shiftable Gaussian BF at 1/2/4/8 B200; % of FP32/HBM roofline"
 UNIT = "Mpixel/s"
 OPS_PER_PX_TERM = 132   # phasor 4 + f*c,f*s 2 + 4 images x 6 line passes x 5 + acc 6
 OPS_PER_PX = 10         # local range ~8 + divide ~2
 L2_FLUSH_BYTES = 256 << 20
+PEAK_FP32_NOMINAL = 148 * 128 * 1.965e9 / 1e12  # T lane-ops/s (FADD/FMUL/FFMA = 1 op)
+DATA = "synthetic (SURVEY.md Appendix A seeded generator; BASELINE names no dataset)"
 
 
 def _cfg_params(cfg):
     from paper_1203_5128_b200.workloads import CONFIGS
     return CONFIGS[cfg]
+
+
+def config_dict(cfg, world):
+    """The workload description printed by BOTH arms (ours / reference)."""
+    p = _cfg_params(cfg)
+    d = dict(workload=p["name"], sigma_s=p["sigma_s"], sigma_r=p["sigma_r"], epsilon=p["epsilon"])
+    if cfg == 4:
+        d.update(images=64, H=4096, W=4096, input_dtype="float32",
+                 parallelism=f"image batch sharded over {world} rank(s) by px*K (LPT), no collective",
+                 l2="no flush: each 64 MiB image and its 128 MiB accumulator exceed what L2 keeps "
+                    "across the batch")
+    elif cfg == 5:
+        d.update(channels=3, H=16384, W=16384, input_dtype="float32",
+                 parallelism=f"row strips over {world} rank(s) with halos, global T by NCCL "
+                             "max all-reduce (3 x fp64, one call)",
+                 l2="no flush: 1 GiB channels")
+    else:
+        n = {1: 512, 2: 1024, 3: 2048}[cfg]
+        d.update(images=1, H=n, W=n,
+                 input_dtype={1: "float64", 2: "float32", 3: "uint16->float32"}[cfg],
+                 parallelism=f"{world} independent replica(s)" if world > 1 else "single GPU",
+                 l2="flushed between timed steps (256 MiB write)")
+    return d
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_distributed(n):
+    """`--gpus N` outside torchrun: run this script under torch.distributed.run
+    with N ranks on 127.0.0.1 and pass its output and exit code through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
 
 
 # ----------------------------------------------------------------------------
@@ -131,7 +177,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------
-# CPU baseline (the oracle port; reference-arm and cpu_baseline leg only)
+# CPU baseline (the oracle port; reference arm and cpu_baseline leg only)
 # ----------------------------------------------------------------------------
 def _cpu_init(barrier):
     os.environ.setdefault("OMP_NUM_THREADS", "1")
@@ -149,53 +195,75 @@ def _cpu_band(args):
     return rows_out * part.shape[1], dt, out["N"], out["M"]
 
 
-def cpu_baseline(cfg=2, min_band_rows=32, max_procs=None):
-    """Time the CPU oracle (float64 C restatement of the reference path,
-    oracle/sbf_oracle.c — bit-identical to the reference on the golden cases
-        and ~2.5x faster than its numpy/Cython original) on the whole image of
-    the config, cut into one band of output rows per host core (halo =
-    support, fixed_T = global T: the strip equivalence of SURVEY.md
-    Appendix C).  Returns (Mpix/s, cores, sample text)."""
-    from oracle import coracle as CO
-    from oracle import shiftbf_oracle as O
-    from paper_1203_5128_b200.workloads import config_image
-    CO.build()
-    p = _cfg_params(cfg)
-    img = config_image(cfg).astype(np.float64)
-    r, a = O.extended_box_params(p["sigma_s"], 3)
-    halo = 3 * (r + (1 if a > 0 else 0))
-    T = CO.compute_T(img, max(1, halo))
-    # whole image when it is small (configs 1, 2), else a leading block of
-    # rows holding ~8 Mpixel (configs 3-5): bounded CPU time and memory
-    H = min(img.shape[0], max(min_band_rows, int(8e6) // img.shape[1]))
-    procs = max(1, min(max_procs or os.cpu_count() or 1, H // min_band_rows))
-    band_rows = -(-H // procs)
-    jobs = []
-    for y0 in range(0, H, band_rows):
-        y1 = min(H, y0 + band_rows)
-        a, b = max(0, y0 - halo), min(img.shape[0], y1 + halo)
-        jobs.append((img[a:b], y1 - y0, T, p))
-    # spawn (the caller holds CUDA threads); workers are started and warmed
-    # before the clock starts, then one band per worker is timed
-    ctx = mp.get_context("spawn")
-    barrier = ctx.Barrier(len(jobs) + 1)
-    with ctx.Pool(len(jobs), initializer=_cpu_init, initargs=(barrier,)) as pool:
+# rows of image/channel 0 the CPU sample covers (None: the whole image)
+_CPU_ROWS = {1: None, 2: None, 3: 128, 4: None, 5: 512}
+
+
+class CpuSample:
+    """The CPU path timed beside the GPU: the C oracle (oracle/sbf_oracle.c,
+    the reference algorithm restated in float64 C; bit-identical to the
+    reference on the golden cases and ~2.5x faster than its numpy/Cython
+    original) on a bounded sample of the workload — image / channel 0 (or its
+    leading rows), cut into one band of output rows per host core (halo =
+    support, fixed_T = the image's global T: the strip equivalence of
+    SURVEY.md Appendix C).  Worker processes are spawned and warmed before
+    any clock starts."""
+
+    def __init__(self, cfg, max_procs=None, min_band_rows=32):
+        from oracle import coracle as CO
+        from oracle import shiftbf_oracle as O
+        from paper_1203_5128_b200.workloads import config_image
+        CO.build()
+        self.p = p = _cfg_params(cfg)
+        img = config_image(cfg).astype(np.float64)
+        r, a = O.extended_box_params(p["sigma_s"], 3)
+        halo = 3 * (r + (1 if a > 0 else 0))
+        T = CO.compute_T(img, max(1, halo))
+        rows = _CPU_ROWS[cfg] or img.shape[0]
+        procs = max(1, min(max_procs or os.cpu_count() or 1, rows // min_band_rows))
+        band = -(-rows // procs)
+        self.jobs = []
+        for y0 in range(0, rows, band):
+            y1 = min(rows, y0 + band)
+            lo, hi = max(0, y0 - halo), min(img.shape[0], y1 + halo)
+            self.jobs.append((img[lo:hi], y1 - y0, T, p))
+        self.procs = len(self.jobs)
+        what = "whole image 0" if rows == img.shape[0] else f"first {rows} rows of image 0"
+        self.desc = (f"C oracle (oracle/sbf_oracle.c, float64) on {what} of {p['name']}: "
+                     f"{self.procs} bands x {band} rows x {img.shape[1]} cols, one process per "
+                     f"band (halo {halo}, fixed global T={T:.6g})")
+        ctx = mp.get_context("spawn")
+        barrier = ctx.Barrier(self.procs + 1)
+        self.pool = ctx.Pool(self.procs, initializer=_cpu_init, initargs=(barrier,))
         barrier.wait()
-        # repeat the sample until ~10 s of CPU work (all cores) have been timed
+
+    def run_once(self):
+        """Mpixel/s of one pass over the sample (wall clock, all bands)."""
         t = time.perf_counter()
-        res = pool.map(_cpu_band, jobs, chunksize=1)
-        reps = 1
-        while (time.perf_counter() - t) * len(jobs) < 10.0 and reps < 8:
-            res = pool.map(_cpu_band, jobs, chunksize=1)
-            reps += 1
+        res = self.pool.map(_cpu_band, self.jobs, chunksize=1)
         wall = time.perf_counter() - t
-    px = reps * sum(x[0] for x in res)
-    what = "whole image" if H == img.shape[0] else f"first {H} rows"
-    sample = (f"C oracle (oracle/sbf_oracle.c, float64), {what}: {len(jobs)} bands x "
-              f"{band_rows} rows x {img.shape[1]} cols of {p['name']} "
-              f"(halo {halo}, fixed global T={T:.6g}, N={res[0][2]}, M={res[0][3]}), "
-              f"{procs} processes, {reps} repetition(s), wall {wall:.2f}s")
-    return px / wall / 1e6, procs, sample
+        self.NM = (res[0][2], res[0][3])
+        return sum(x[0] for x in res) / wall / 1e6, wall
+
+    def close(self):
+        self.pool.terminate()
+        self.pool.join()
+
+
+def cpu_baseline(cfg, min_seconds=10.0, max_reps=8):
+    s = CpuSample(cfg)
+    try:
+        vals, total = [], 0.0
+        while total * s.procs < min_seconds and len(vals) < max_reps:
+            v, wall = s.run_once()
+            vals.append(v)
+            total += wall
+        v = float(np.median(vals))
+        sample = (f"{s.desc}, N={s.NM[0]}, M={s.NM[1]}, {len(vals)} repetition(s) "
+                  f"(median), {total:.1f}s wall")
+        return dict(value=v, unit=UNIT, cores=s.procs, kind="port", sample=sample)
+    finally:
+        s.close()
 
 
 # ----------------------------------------------------------------------------
@@ -217,18 +285,97 @@ def fp32_peak(lib, torch, dev, packed=False):
         e1.synchronize()
         ms = e0.elapsed_time(e1)
         best = max(best, blocks * threads * iters * (16 if packed else 8) / (ms * 1e-3))
-    return best / 1e12, sms
+    return best / 1e12
 
 
-def load_profile_traffic():
-    """dram bytes per K3 launch from the committed ncu --set full summary."""
-    path = os.path.join(REPO, "profiles", "k3_traffic.json")
+def profile_traffic(cfg):
+    """DRAM bytes per K3 launch from the committed ncu --set full summary of
+    this workload (profiles/k3_traffic_cfg<N>.json), or None."""
+    path = os.path.join(REPO, "profiles", f"k3_traffic_cfg{cfg}.json")
     try:
         with open(path) as fh:
-            d = json.load(fh)
-        return d.get("dram_bytes_per_launch")
+            return json.load(fh).get("dram_bytes_per_launch")
     except Exception:
         return None
+
+
+def _max_over_ranks(torch, dev, world, *vals):
+    t = torch.tensor(list(vals), dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
+class Pipeline:
+    """Device-resident sbf_shiftable_bf calls on a set of images, rotating
+    over `lanes` streams (own workspace and meta block per image slot)."""
+
+    def __init__(self, torch, dev, imgs, params, lanes):
+        from paper_1203_5128_b200 import _lib
+        from paper_1203_5128_b200.kernels import log_2_over_eps
+        from paper_1203_5128_b200.spatial import to_c_spatial
+        self.torch, self._lib, self.lib = torch, _lib, _lib.load()
+        self.imgs = imgs
+        self.params = params
+        self.sp = to_c_spatial(params.resolved_spatial())
+        self.R = params.resolved_radius()
+        self.l2e = log_2_over_eps(params.epsilon)
+        self.dts = [_lib.SBF_F64 if f.dtype == torch.float64 else _lib.SBF_F32 for f in imgs]
+        self.outs = [torch.empty(f.shape, dtype=f.dtype, device=dev) for f in imgs]
+        self.meta = torch.empty((len(imgs), 256), dtype=torch.uint8, device=dev)
+        self.main = torch.cuda.current_stream()
+        self.lanes = []
+        for k in range(max(1, lanes)):
+            H, W = imgs[0].shape
+            ws = self.lib.sbf_shiftable_bf_workspace(H, W, self.dts[0], self.sp, _lib.PREC_FP32,
+                                                     1 << 16)
+            self.lanes.append(dict(stream=torch.cuda.Stream(device=dev) if lanes > 1 else self.main,
+                                   ws=torch.empty(ws, dtype=torch.uint8, device=dev)))
+
+    def launch(self, i, lane):
+        _lib, p, f = self._lib, self.params, self.imgs[i]
+        H, W = f.shape
+        m = self.meta[i].data_ptr()
+        _lib.check(self.lib.sbf_shiftable_bf(
+            f.data_ptr(), self.dts[i], H, W, self.sp, self.R, -1.0, p.sigma_r, p.epsilon, 0,
+            self.l2e, _lib.PREC_FP32, self.outs[i].data_ptr(), self.dts[i], m, m + 128, m + 64,
+            1 << 16, lane["ws"].data_ptr(), lane["ws"].numel(), lane["stream"].cuda_stream))
+
+    def step(self):
+        ev = self.torch.cuda.Event()
+        ev.record(self.main)
+        for ln in self.lanes:
+            if ln["stream"] is not self.main:
+                ln["stream"].wait_event(ev)
+        for i in range(len(self.imgs)):
+            self.launch(i, self.lanes[i % len(self.lanes)])
+        for ln in self.lanes:
+            if ln["stream"] is not self.main:
+                self.main.wait_stream(ln["stream"])
+
+    def k3_times(self):
+        """Each image alone on the main stream with events around its K3
+        launch: [(K3 ms, K_eval)] (the dominant kernel's per-launch time)."""
+        torch, lib = self.torch, self.lib
+        lane = dict(stream=self.main, ws=self.lanes[0]["ws"])
+        evs = []
+        for i in range(len(self.imgs)):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(self.main)
+            b.record(self.main)  # materialise the handles
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        for i, (a, b) in enumerate(evs):
+            lib.sbf_set_k3_events(a.cuda_event, b.cuda_event)
+            self.launch(i, lane)
+            lib.sbf_set_k3_events(None, None)
+        torch.cuda.synchronize()
+        plans = self.plans()
+        return [(a.elapsed_time(b), pl.K_eval) for (a, b), pl in zip(evs, plans)]
+
+    def plans(self):
+        raw = self.meta.cpu().numpy()
+        return [self._lib.SbfPlan.from_buffer_copy(raw[i, :64].tobytes()) for i in range(len(raw))]
 
 
 def run_ours(args, rank, world, dev):
@@ -236,242 +383,119 @@ def run_ours(args, rank, world, dev):
 
     import paper_1203_5128_b200 as P
     from paper_1203_5128_b200 import _lib
-    from paper_1203_5128_b200.kernels import log_2_over_eps
-    from paper_1203_5128_b200.spatial import to_c_spatial
-    from paper_1203_5128_b200.workloads import config_image
+    from paper_1203_5128_b200.dist import shard_images
+    from paper_1203_5128_b200.workloads import CFG4_K, config_image, generate_many
 
     lib = _lib.load()
-    p = _cfg_params(args.config)
-    img_np = config_image(args.config)
-    H, W = img_np.shape
-    f = torch.from_numpy(np.ascontiguousarray(img_np)).to(dev)
-    dt = _lib.SBF_F64 if f.dtype == torch.float64 else _lib.SBF_F32
-    # default parameters, as a user calls it (precision "auto": fp32 kernels
-    # with the device-side HDR guard); the device-resident step below passes
-    # SBF_PREC_FP32 explicitly, which runs the same kernels
+    cfg = args.config
+    p = _cfg_params(cfg)
     params = P.FilterParams(sigma_s=p["sigma_s"], sigma_r=p["sigma_r"], epsilon=p["epsilon"])
-    sp = to_c_spatial(params.resolved_spatial())
-    R = params.resolved_radius()
-    prec = _lib.PREC_FP32
-    cap = 1 << 16
-    stats = torch.empty(8, dtype=torch.float64, device=dev)
-    plan = torch.empty(64, dtype=torch.uint8, device=dev)
-    out = torch.empty((H, W), dtype=torch.float32, device=dev)
-    fb = torch.zeros(1, dtype=torch.int64, device=dev)
-    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
-    st = torch.cuda.current_stream()
-    sptr = st.cuda_stream
-    l2e = log_2_over_eps(p["epsilon"])
-
-    # one step = the fused device pipeline (sbf_shiftable_bf: K1 with the plan
-    # and the accumulator clear folded in, K3, K4, programmatic dependent
-    # launches); events 2/3 are recorded by the library around the K3 launch
-    pws = torch.empty(lib.sbf_shiftable_bf_workspace(H, W, dt, sp, prec, cap), dtype=torch.uint8,
-                      device=dev)
-
-    def step(evs=None):
-        if evs is not None:
-            evs[0].record(st)
-            lib.sbf_set_k3_events(evs[2].cuda_event, evs[3].cuda_event)
-        _lib.check(lib.sbf_shiftable_bf(f.data_ptr(), dt, H, W, sp, R, -1.0, p["sigma_r"],
-                                        p["epsilon"], 0, l2e, prec, out.data_ptr(), _lib.SBF_F32,
-                                        plan.data_ptr(), stats.data_ptr(), fb.data_ptr(), cap,
-                                        pws.data_ptr(), pws.numel(), sptr))
-        if evs is not None:
-            lib.sbf_set_k3_events(None, None)
-            evs[4].record(st)
+    if cfg == 4:
+        # balance ranks by px * K (K per image from the reference
+        # plan table, identical on every rank: no communication)
+        parts = shard_images([float(k) for k in CFG4_K[:args.images]], world)
+        mine = parts[rank]
+        host = [np.ascontiguousarray(a) for a in generate_many(4, mine)]
+        flush = None
+    else:
+        mine = [0]
+        host = [np.ascontiguousarray(config_image(cfg))]
+        flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    imgs = [torch.from_numpy(a).to(dev) for a in host]
+    pipe = Pipeline(torch, dev, imgs, params, args.lanes if cfg == 4 else 1)
+    st = pipe.main
 
     for _ in range(args.warmup):
-        step()
-        flush.zero_()
-    torch.cuda.synchronize()
-    planc = _lib.SbfPlan.from_buffer_copy(plan.cpu().numpy().tobytes())
-    # parity spot check of the benchmarked output (cheap invariants)
-    o = out.cpu().numpy()
-    assert np.isfinite(o).all() and o.min() >= img_np.min() - 1e-3 and o.max() <= img_np.max() + 1e-3
-
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    evsets = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
-    for es in evsets:  # materialise the event handles handed to the library
-        for e in es:
-            e.record(st)
-    torch.cuda.synchronize()
-    with ClockSampler(dev.index if dev.index is not None else 0) as clk:
-        for k in range(args.steps):
-            step(evsets[k])
+        pipe.step()
+        if flush is not None:
             flush.zero_()
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    plans = pipe.plans()
+    # cheap invariants of the benchmarked outputs (parity is in tests/)
+    for a, o in zip(host, pipe.outs):
+        o = o.cpu().numpy()
+        assert np.isfinite(o).all() and o.min() >= a.min() - 1e-3 and o.max() <= a.max() + 1e-3
+
     if world > 1:
         torch.distributed.barrier()
-    step_ms = [e[0].elapsed_time(e[4]) for e in evsets]
-    k3_ms = [e[2].elapsed_time(e[3]) for e in evsets]
-    k1_ms = [e[0].elapsed_time(e[2]) for e in evsets]  # K1 (+ fused plan / clear)
-    total_ms = float(np.sum(step_ms))
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with ClockSampler(dev.index if dev.index is not None else 0) as clk:
+        for a, b in evs:
+            a.record(st)
+            pipe.step()
+            b.record(st)
+            if flush is not None:
+                flush.zero_()
+        torch.cuda.synchronize()
+    step_ms = float(np.sum([a.elapsed_time(b) for a, b in evs]))
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    px = H * W
-    value = world * px * args.steps / (total_ms * 1e-3) / 1e6
+        torch.distributed.barrier()
 
-    # e2e through the public API from pinned host memory (input H2D + result D2H)
-    pinned = torch.from_numpy(np.ascontiguousarray(img_np)).pin_memory()
-    res = None
-    for _ in range(max(3, args.warmup)):
-        # keep the previous result alive exactly like the timed loop, so the
-        # pinned-host caching allocator holds both result blocks before timing
-        res = P.shiftable_bf(pinned, params)
+    # the dominant kernel alone, per launch (K3 term sweep + fused epilogue)
+    k3 = pipe.k3_times()
+    px = [int(f.shape[0] * f.shape[1]) for f in imgs]
+    k3_ms = float(sum(t for t, _ in k3))
+    k3_ops = float(sum(OPS_PER_PX_TERM * n * k for n, (_, k) in zip(px, k3)))
+
+    # end to end through the public API: page-locked host images in, results
+    # written into page-locked host memory, every byte inside the timed region
+    pinned_in = [torch.from_numpy(a).pin_memory() for a in host]
+    pinned_out = [torch.empty(a.shape, dtype=t.dtype, pin_memory=True) for a, t in zip(host, imgs)]
+    for _ in range(max(1, min(args.warmup, 2))):
+        P.shiftable_bf_batch(pinned_in, params, lanes=args.lanes, out=pinned_out)
     torch.cuda.synchronize()
     gc.collect()
     gc.disable()  # no collector pauses inside the timed region
-    e2e_ms = []
-    for _ in range(args.steps):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        res = P.shiftable_bf(pinned, params)
-        e1.record(st)
-        e1.synchronize()
-        e2e_ms.append(e0.elapsed_time(e1))
-        flush.zero_()
-    gc.enable()
-    e2e_total = float(np.sum(e2e_ms))
-    if world > 1:
-        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_total = float(t.item())
-    e2e_value = world * px * args.steps / (e2e_total * 1e-3) / 1e6
-    h2d = img_np.nbytes
-    # result (the input's float dtype for torch input) + plan + stats + fallback counter
-    d2h = px * res.image.element_size() + 64 + 64 + 8
-
-    peak_meas, sms = fp32_peak(lib, torch, dev)
-    peak_meas2, _ = fp32_peak(lib, torch, dev, packed=True)
-    peak_nominal = sms * 128 * 1.965e9 / 1e12
-    k3_avg = float(np.mean(k3_ms))
-    ops = OPS_PER_PX_TERM * px * planc.K_eval
-    achieved = ops / (k3_avg * 1e-3) / 1e12
-    geo = ctypes_int7()
-    lib.sbf_filter_geometry(H, W, sp, prec, geo)
-    return dict(
-        value=value, ms_per_step=ms_per_step, planc=planc, k3_avg=k3_avg, k1_avg=float(np.mean(k1_ms)),
-        e2e=dict(value=e2e_value, unit=UNIT, h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h),
-                 ms_per_step=e2e_total / args.steps),
-        roofline=dict(bound="fp32", achieved=achieved, peak=peak_nominal, unit="TFLOP/s",
-                      frac=achieved / peak_nominal, traffic=load_profile_traffic(),
-                      peak_source="nominal 148 SM x 128 FP32 lanes x 1.965 GHz (ops: FADD/FMUL/FFMA = 1)",
-                      peak_measured_ffma=peak_meas, peak_measured_ffma2=peak_meas2,
-                      frac_of_measured=achieved / max(peak_meas, peak_meas2),
-                      kernel="sbf::terms_kernel<4,3,0> (K3)",
-                      ops_per_launch=ops, ops_basis=f"{OPS_PER_PX_TERM} ops/px/evaluated term x {px} px x {planc.K_eval} terms"),
-        clocks=clk.summary(), geometry=list(geo), W=W, H=H, p=p)
-
-
-def _device_plan_cost(lib, torch, f, params, dev):
-    """(K_eval of the image's plan) — used to balance the config-4 shards."""
-    import paper_1203_5128_b200 as P
-    res = P.shiftable_bf(f, params)
-    return res.plan.N // 2 - res.plan.M + 1
-
-
-def run_batch(args, rank, world, dev):
-    """Config 4: a batch of independent images sharded across ranks."""
-    import torch
-
-    import paper_1203_5128_b200 as P
-    from paper_1203_5128_b200 import _lib
-    from paper_1203_5128_b200.dist import shard_images
-    from paper_1203_5128_b200.kernels import log_2_over_eps
-    from paper_1203_5128_b200.spatial import to_c_spatial
-    from paper_1203_5128_b200.workloads import config_image
-
-    lib = _lib.load()
-    p = _cfg_params(args.config)
-    n_img = args.images
-    params = P.FilterParams(sigma_s=p["sigma_s"], sigma_r=p["sigma_r"], epsilon=p["epsilon"])
-    sp = to_c_spatial(params.resolved_spatial())
-    R = params.resolved_radius()
-    # SURVEY §8(e): balance ranks by px * K.  Every rank plans every image
-    # (K1 + host plan twin, outside the timed region) so the LPT sharding is
-    # identical on all ranks without communication.
-    ks_all = []
-    for i in range(n_img):
-        g = torch.from_numpy(np.ascontiguousarray(config_image(4, i))).to(dev)
-        pl = P.select_plan(P.compute_T(g, R), p["sigma_r"], p["epsilon"])
-        ks_all.append(pl.N // 2 - pl.M + 1)
-        del g
-    parts = shard_images([float(k) for k in ks_all], world)
-    mine = parts[rank]
-    imgs = [torch.from_numpy(np.ascontiguousarray(config_image(4, i))).to(dev) for i in mine]
-    H, W = imgs[0].shape
-    cap = 1 << 16
-    st = torch.cuda.current_stream()
-    l2e = log_2_over_eps(p["epsilon"])
-    # images alternate between `lanes` streams (own workspace, plan, stats):
-    # one image's K1 and K3 start fills the SMs the previous image's K3
-    # leaves idle while its last items finish
-    lanes = []
-    for _ in range(max(1, args.lanes)):
-        lanes.append(dict(
-            stream=torch.cuda.Stream(device=dev) if args.lanes > 1 else st,
-            ws=torch.empty(lib.sbf_shiftable_bf_workspace(H, W, _lib.SBF_F32, sp, _lib.PREC_FP32,
-                                                          cap), dtype=torch.uint8, device=dev),
-            stats=torch.empty(8, dtype=torch.float64, device=dev),
-            plan=torch.empty(64, dtype=torch.uint8, device=dev),
-            fb=torch.zeros(1, dtype=torch.int64, device=dev)))
-    outs = [torch.empty((H, W), dtype=torch.float32, device=dev) for _ in mine]
-
-    def step():
-        for i, (f, o) in enumerate(zip(imgs, outs)):
-            ln = lanes[i % len(lanes)]
-            _lib.check(lib.sbf_shiftable_bf(f.data_ptr(), _lib.SBF_F32, H, W, sp, R, -1.0,
-                                            p["sigma_r"], p["epsilon"], 0, l2e, _lib.PREC_FP32,
-                                            o.data_ptr(), _lib.SBF_F32, ln["plan"].data_ptr(),
-                                            ln["stats"].data_ptr(), ln["fb"].data_ptr(), cap,
-                                            ln["ws"].data_ptr(), ln["ws"].numel(),
-                                            ln["stream"].cuda_stream))
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev.index or 0) as clk:
-        e0.record(st)
-        for ln in lanes:
-            ln["stream"].wait_event(e0)
-        for _ in range(args.steps):
-            step()
-        for ln in lanes:
-            st.wait_stream(ln["stream"])
-        e1.record(st)
-        e1.synchronize()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    total = float(t.item())
-    px = n_img * H * W
-    # algorithmic FP32 ops of the whole batch (SURVEY §8(d): 132 per pixel per
-    # evaluated folded term); K per image from the host twin of the plan
-    kt = torch.tensor([float(sum(ks_all))], dtype=torch.float64)
-    ops = OPS_PER_PX_TERM * H * W * float(kt.item())
-    achieved = ops * args.steps / (total * 1e-3) / 1e12
-    peak = 148 * 128 * 1.965e9 / 1e12
-    return dict(value=px * args.steps / (total * 1e-3) / 1e6, ms_per_step=total / args.steps,
-                launches=KERNELS_PER_IMAGE * len(mine) * args.steps, clocks=clk.summary(),
-                roofline=dict(bound="fp32", achieved=achieved, peak=peak * world, unit="TFLOP/s",
-                              frac=achieved / (peak * world), traffic=None,
-                              kernel="whole step (K1..K4 over the batch, all ranks)",
-                              ops_basis=f"{OPS_PER_PX_TERM} ops/px/term x {H}x{W} px x sum K = {int(kt.item())}"),
-                config=dict(workload=p["name"], images=n_img, H=H, W=W, sigma_s=p["sigma_s"],
-                            sigma_r=p["sigma_r"], epsilon=p["epsilon"],
-                            parallelism=f"image batch sharded over {world} rank(s) by px*K (LPT), no collective",
-                            sum_K=int(sum(ks_all)), rank_K=[int(sum(ks_all[i] for i in part)) for part in parts],
-                            l2="inputs (64 MiB/image) exceed what L2 keeps across images"))
+    e2e_ms = 0.0
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        res = P.shiftable_bf_batch(pinned_in, params, lanes=args.lanes, out=pinned_out)
+        b.record(st)
+        b.synchronize()
+        e2e_ms += a.elapsed_time(b)
+        if flush is not None:
+            flush.zero_()
+    gc.enable()
+    assert all((r.plan.N, r.plan.M) == (pl.N, pl.M) for r, pl in zip(res, plans))
+    h2d = sum(a.nbytes for a in host)
+    d2h = sum(o.numel() * o.element_size() for o in pinned_out) + 256 * len(host)
+
+    step_ms, e2e_ms, k3_ms_max = _max_over_ranks(torch, dev, world, step_ms, e2e_ms, k3_ms)
+    total_px = args.images * 4096 * 4096 if cfg == 4 else world * px[0]
+    value = total_px * args.steps / (step_ms * 1e-3) / 1e6
+    e2e_value = total_px * args.steps / (e2e_ms * 1e-3) / 1e6
+    peak2 = fp32_peak(lib, torch, dev, packed=True)
+    achieved = k3_ops / (k3_ms * 1e-3) / 1e12
+    sum_k = sum(k for _, k in k3)
+    step_ops = OPS_PER_PX_TERM * sum(n * k for n, (_, k) in zip(px, k3)) + OPS_PER_PX * sum(px)
+    return dict(
+        value=value, ms_per_step=step_ms / args.steps, clocks=clk.summary(),
+        launches=KERNELS_PER_IMAGE * len(imgs) * args.steps,
+        e2e=dict(value=e2e_value, unit=UNIT, h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h),
+                 ms_per_step=e2e_ms / args.steps,
+                 path="shiftable_bf_batch: pinned host images -> copy-engine H2D per stream, "
+                      "results stored by the K3 epilogue straight into pinned host memory"),
+        roofline=dict(
+            bound="fp32", achieved=achieved, peak=PEAK_FP32_NOMINAL, unit="TFLOP/s",
+            frac=achieved / PEAK_FP32_NOMINAL, traffic=profile_traffic(cfg),
+            peak_source="nominal 148 SM x 128 FP32 lanes x 1.965 GHz (FADD/FMUL/FFMA = 1 op); "
+                        "MEASURED_PEAKS.json has no FP32 entry",
+            peak_measured_ffma2=peak2, frac_of_measured=achieved / peak2,
+            kernel="K3 term sweep + fused epilogue, each image alone on one stream (CUDA events)",
+            ops_per_launch=k3_ops / len(k3), k3_ms_per_launch=k3_ms / len(k3),
+            ops_basis=f"{OPS_PER_PX_TERM} ops/px/evaluated term x {px[0]} px x K_eval "
+                      f"(sum over this rank's {len(k3)} image(s) = {sum_k})",
+            traffic_source=f"profiles/k3_traffic_cfg{cfg}.json (ncu --set full)"),
+        step_roofline=dict(achieved=step_ops * args.steps / (step_ms * 1e-3) / 1e12 * world,
+                           frac=step_ops * args.steps / (step_ms * 1e-3) / 1e12 * world
+                           / (PEAK_FP32_NOMINAL * world),
+                           note="whole step (all kernels, all ranks) against world x nominal peak"),
+        plans=[(float(pl.T), int(pl.N), int(pl.M), int(pl.K_eval)) for pl in plans[:4]])
 
 
 def run_strips(args, rank, world, dev):
@@ -483,7 +507,7 @@ def run_strips(args, rank, world, dev):
     from paper_1203_5128_b200.workloads import config_image
 
     p = _cfg_params(args.config)
-    size = args.size or 16384
+    size = 16384
     params = P.FilterParams(sigma_s=p["sigma_s"], sigma_r=p["sigma_r"], epsilon=p["epsilon"])
     s = strip_plan(size, world, strip_halo(params))[rank]
     bufs = []
@@ -505,78 +529,62 @@ def run_strips(args, rank, world, dev):
             sf.run()
         e1.record(st)
         e1.synchronize()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    total = float(t.item())
+    total, = _max_over_ranks(torch, dev, world, e0.elapsed_time(e1))
     px = 3 * size * size
     plans = sf.plans_host()
-    # r >= 9 runs the split sweep: K1 (2) + plan + 2 kernels per term + K4
-    r_sp, _ = P.extended_box_params(p["sigma_s"], 3)
-    if r_sp >= 9:
-        per_step = sum(3 + 2 * (pl.N // 2 - pl.M + 1) + 1 for pl in plans)
-    else:
-        per_step = KERNELS_STRIP_IMAGE * 3
     ops = OPS_PER_PX_TERM * size * size * sum(pl.N // 2 - pl.M + 1 for pl in plans)
     achieved = ops * args.steps / (total * 1e-3) / 1e12
-    peak = 148 * 128 * 1.965e9 / 1e12 * world
+    peak = PEAK_FP32_NOMINAL * world
     return dict(value=px * args.steps / (total * 1e-3) / 1e6, ms_per_step=total / args.steps,
-                launches=per_step * args.steps, clocks=clk.summary(),
+                launches=sf.launches_per_run() * args.steps, clocks=clk.summary(),
                 roofline=dict(bound="fp32", achieved=achieved, peak=peak, unit="TFLOP/s",
-                              frac=achieved / peak, traffic=None,
-                              kernel="whole step (K1, plan, split sweep / K3, K4; 3 channels, all ranks)",
+                              frac=achieved / peak, traffic=profile_traffic(5),
+                              kernel="whole step (K1, plan, term sweeps, epilogue; 3 channels, all ranks)",
                               ops_basis=f"{OPS_PER_PX_TERM} ops/px/term x {size}^2 px x sum K over channels"),
-                config=dict(workload=p["name"], channels=3, H=size, W=size, sigma_s=p["sigma_s"],
-                            sigma_r=p["sigma_r"], epsilon=p["epsilon"],
-                            plans=[(pl.T, pl.N, pl.M) for pl in plans],
-                            parallelism=f"row strips over {world} rank(s), halo {s.out_lo - s.buf_lo or s.buf_hi - s.out_hi} rows, "
-                                        "global T by NCCL max-allreduce (3 x fp64, one call)"))
-
-
-def ctypes_int7():
-    import ctypes
-    return (ctypes.c_int * 7)()
+                plans=[(pl.T, pl.N, pl.M) for pl in plans])
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--images", type=int, default=64, help="config 4 batch size")
     ap.add_argument("--lanes", type=int, default=3,
-                    help="config 4: streams the images alternate on (1: 6043, 2: 6118, 3: 6170, 6: 6078 Mpix/s); config 5: > 1 runs each channel on its own stream")
-    ap.add_argument("--size", type=int, default=None, help="config 5 side (default 16384)")
+                    help="streams the images rotate over (config 4); > 1: one stream per channel (config 5)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    p = _cfg_params(args.config)
+    cfgd = config_dict(args.config, world)
 
     if args.impl == "reference":
-        # the reference's CPU path (oracle port; the Python reference cannot
-        # travel to the box) on the host cores, rank 0 only
+        # the reference's CPU path (oracle port: the Python reference cannot
+        # travel to the GPU box) on all host cores, rank 0 only; each step is
+        # one pass over a bounded sample of the workload
         if rank != 0:
             return
-        vals = []
-        for _ in range(args.warmup):
-            pass  # the port has no warm-up state; warm-up steps are not timed
-        for k in range(args.steps):
-            v, cores, sample = cpu_baseline(args.config, max_procs=None)
-            vals.append(v)
+        s = CpuSample(args.config)
+        try:
+            for _ in range(args.warmup):
+                s.run_once()
+            vals = [s.run_once()[0] for _ in range(args.steps)]
+        finally:
+            s.close()
         v = float(np.median(vals))
-        line = dict(metric=METRIC, value=v, unit=UNIT, n_gpus=args.gpus, steps=args.steps,
-                    warmup=args.warmup, ms_per_step=None, higher_is_better=True, scaling="weak",
-                    vs_baseline=None, dtype="f64", data="synthetic (SURVEY.md Appendix A generator)",
-                    config=dict(workload=p["name"], sigma_s=p["sigma_s"], sigma_r=p["sigma_r"],
-                                epsilon=p["epsilon"]),
-                    impl="reference",
-                    cpu_baseline=dict(value=v, unit=UNIT, cores=cores, kind="port", sample=sample),
+        line = dict(metric=METRIC, value=v, unit=UNIT, n_gpus=world, steps=args.steps,
+                    warmup=args.warmup, ms_per_step=None, higher_is_better=True,
+                    scaling="strong" if args.config in (4, 5) else "weak", vs_baseline=None,
+                    dtype="f64", data=DATA, config=cfgd, impl="reference",
+                    cpu_baseline=dict(value=v, unit=UNIT, cores=s.procs, kind="port",
+                                      sample=f"{s.desc}, N={s.NM[0]}, M={s.NM[1]}; median of "
+                                             f"{args.steps} passes"),
                     e2e=dict(value=v, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
         print(json.dumps(line))
         return
@@ -587,46 +595,23 @@ def main():
         torch.distributed.init_process_group("nccl")
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
-    if args.config in (4, 5):
-        r = (run_batch if args.config == 4 else run_strips)(args, rank, world, dev)
-        if world > 1:
-            torch.distributed.barrier()
-            torch.distributed.destroy_process_group()
-        if rank == 0:
-            line = dict(metric=METRIC, value=r["value"], unit=UNIT, n_gpus=world, steps=args.steps,
-                        warmup=args.warmup, ms_per_step=r["ms_per_step"], higher_is_better=True,
-                        scaling="strong", vs_baseline=None,
-                        dtype="f32", data="synthetic (SURVEY.md Appendix A generator, seeded)",
-                        config=r["config"], roofline=r.get("roofline"),
-                        gpu_launches=r["launches"], clocks=r["clocks"])
-            print(json.dumps(line))
-        return
-    r = run_ours(args, rank, world, dev)
+    r = (run_strips if args.config == 5 else run_ours)(args, rank, world, dev)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, cores, sample = cpu_baseline(args.config)
-        cpu = dict(value=v, unit=UNIT, cores=cores, kind="port", sample=sample)
+        cpu = cpu_baseline(args.config)
     if world > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
     if rank != 0:
         return
-    pl = r["planc"]
-    geo = r["geometry"]
-    line = dict(
-        metric=METRIC, value=r["value"], unit=UNIT, n_gpus=world, steps=args.steps,
-        warmup=args.warmup, ms_per_step=r["ms_per_step"], higher_is_better=True, scaling="weak",
-        vs_baseline=None, dtype="f32",
-        data="synthetic (SURVEY.md Appendix A generator, seeded; BASELINE names no dataset)",
-        config=dict(workload=p["name"], H=r["H"], W=r["W"], sigma_s=p["sigma_s"],
-                    sigma_r=p["sigma_r"], epsilon=p["epsilon"], T=pl.T, N=pl.N, M=pl.M, K=pl.K,
-                    K_eval=pl.K_eval, parallelism=("replicas" if world > 1 else "single"),
-                    l2="flushed between timed steps (256 MiB write)",
-                    k3_geometry=dict(halo=geo[0], out_cols_per_strip=geo[1], threads=geo[2],
-                                     band_rows=geo[3], strips=geo[4], bands=geo[5], groups=geo[6]),
-                    k3_ms=r["k3_avg"], k1_ms=r["k1_avg"]),
-        roofline=r["roofline"], cpu_baseline=cpu, e2e=r["e2e"],
-        gpu_launches=KERNELS_PER_IMAGE * args.steps, clocks=r["clocks"])
+    line = dict(metric=METRIC, value=r["value"], unit=UNIT, n_gpus=world, steps=args.steps,
+                warmup=args.warmup, ms_per_step=r["ms_per_step"], higher_is_better=True,
+                scaling="strong" if args.config in (4, 5) else "weak", vs_baseline=None,
+                dtype="f32", data=DATA, config=cfgd, roofline=r["roofline"], cpu_baseline=cpu,
+                e2e=r.get("e2e"), gpu_launches=r["launches"], clocks=r["clocks"])
+    for k in ("step_roofline", "plans"):
+        if k in r:
+            line[k] = r[k]
     print(json.dumps(line))
 
 

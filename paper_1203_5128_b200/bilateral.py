@@ -21,7 +21,6 @@ from . import _lib
 from .errors import InvalidParameterError
 from .image import stage
 from .kernels import KernelFamily, KernelPlan, log_2_over_eps, select_plan
-from .maxfilter import _stream_ptr
 from .spatial import IteratedBox, SpatialMode, support_radius, to_c_spatial
 
 TERMS_CAP = 1 << 16
@@ -165,6 +164,16 @@ def _scratch(dev, ws_bytes):
 
 
 def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False):
+    """Runs `_filter_on_device` with the image's device current, so the
+    library's per-device caches, the stream and the workspace all belong to
+    the device that holds the data (a tensor on a non-current GPU)."""
+    import torch
+
+    with torch.cuda.device(s.tensor.device):
+        return _filter_on_device(s, params, out_f64, to_host)
+
+
+def _filter_on_device(s, params: FilterParams, out_f64: bool, to_host: bool = False):
     """K1..K4 on a staged device image; returns (output, KernelPlan, fallbacks).
 
     One C call (sbf_shiftable_bf) launches the whole pipeline without a host
@@ -187,7 +196,7 @@ def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False
     if use_fixed and not float(params.fixed_T) >= 0.0:
         raise InvalidParameterError("T must be non-negative")  # kernels.py:118-119
     prec = _precision_code(params)
-    stream = _stream_ptr()
+    stream = torch.cuda.current_stream(dev).cuda_stream
     rule = _lib.RULES.get(params.truncation, -1)
     l2e = log_2_over_eps(params.epsilon)
     total, terms_off, fws_off = _workspace_layout(
@@ -242,6 +251,112 @@ def _filter_staged(s, params: FilterParams, out_f64: bool, to_host: bool = False
                                                   TERMS_CAP, stream), "plan")
             plan_c, fallbacks = rerun()
     return out, _plan_from_struct(plan_c), fallbacks
+
+
+def shiftable_bf_batch(imgs, params: FilterParams, lanes: int = 3, out=None):
+    """`[shiftable_bf(img, params) for img in imgs]`, pipelined on the GPU.
+
+    A batch of independent images (the config-4 workload) is the same call
+    repeated, so each result equals the single-image call bit for bit (same
+    kernels, same plan).  What changes is the schedule: images rotate over
+    `lanes` CUDA streams, each with its own workspace, so one image's
+    host->device copy (copy engine), another's kernels and a third's result
+    write-back over PCIe (the epilogue stores straight into page-locked
+    memory) overlap.  One host synchronisation for the whole batch reads
+    every plan, fallback count and statistics block back.
+
+    `imgs`: torch tensors — page-locked host tensors (float32/float64) or
+    CUDA tensors; other inputs go through `shiftable_bf` one by one.
+    `out`: optional list of result tensors (same shape, float dtype of the
+    input, same side) to write into.
+    """
+    import torch
+
+    imgs = list(imgs)
+    fast = all(isinstance(t, torch.Tensor) and t.ndim == 2 and t.numel() > 0 and
+               t.dtype in (torch.float32, torch.float64) and t.is_contiguous() and
+               (t.is_cuda or t.is_pinned()) for t in imgs)
+    if not fast or params.family is KernelFamily.POLYNOMIAL or not imgs:
+        return [shiftable_bf(t, params) for t in imgs]
+    lib = _lib.load()
+    sp = to_c_spatial(params.resolved_spatial())
+    radius = params.resolved_radius()
+    use_fixed = params.fixed_T is not None
+    if use_fixed and not float(params.fixed_T) >= 0.0:
+        raise InvalidParameterError("T must be non-negative")
+    prec = _precision_code(params)
+    rule = _lib.RULES.get(params.truncation, -1)
+    l2e = log_2_over_eps(params.epsilon)
+    dev = next((t.device for t in imgs if t.is_cuda), None)
+    dev = dev if dev is not None else torch.device("cuda", torch.cuda.current_device())
+    n = len(imgs)
+    lanes = max(1, min(int(lanes), n))
+    metas = torch.empty((n, _META_BYTES), dtype=torch.uint8, device=dev)
+    metas_h = torch.empty((n, _META_BYTES), dtype=torch.uint8, pin_memory=True)
+    outs = list(out) if out is not None else [
+        torch.empty(t.shape, dtype=t.dtype, **({"device": dev} if t.is_cuda else {"pin_memory": True}))
+        for t in imgs]
+    with torch.cuda.device(dev):
+        main = torch.cuda.current_stream(dev)
+        start = torch.cuda.Event()
+        start.record(main)
+        lane = []
+        for _ in range(lanes):
+            s = torch.cuda.Stream(device=dev)
+            s.wait_event(start)
+            lane.append({"stream": s, "ws": None, "inp": None})
+        for i, (t, o) in enumerate(zip(imgs, outs)):
+            ln = lane[i % lanes]
+            H, W = int(t.shape[0]), int(t.shape[1])
+            dt = _lib.SBF_F64 if t.dtype == torch.float64 else _lib.SBF_F32
+            total, _, _ = _workspace_layout(H, W, dt, (sp.mode, sp.passes, sp.r, 0, sp.alpha,
+                                                      sp.sigma_s), prec)
+            with torch.cuda.stream(ln["stream"]):
+                if ln["ws"] is None or ln["ws"].numel() < total:
+                    ln["ws"] = torch.empty(total, dtype=torch.uint8, device=dev)
+                src = t
+                if not t.is_cuda:
+                    # copy engine, stream-ordered on the lane: overlaps the
+                    # other lanes' kernels without taking SMs
+                    b = ln["inp"]
+                    if b is None or b.shape != t.shape or b.dtype != t.dtype:
+                        b = ln["inp"] = torch.empty(t.shape, dtype=t.dtype, device=dev)
+                    b.copy_(t, non_blocking=True)
+                    src = b
+                m = metas[i]
+                _lib.check(lib.sbf_shiftable_bf(
+                    src.data_ptr(), dt, H, W, sp, radius,
+                    float(params.fixed_T) if use_fixed else -1.0, float(params.sigma_r),
+                    float(params.epsilon), rule, l2e, prec, o.data_ptr(),
+                    _lib.SBF_F64 if o.dtype == torch.float64 else _lib.SBF_F32,
+                    m.data_ptr() + _META_PLAN, m.data_ptr() + _META_STATS,
+                    m.data_ptr() + _META_FB, TERMS_CAP, ln["ws"].data_ptr(), total,
+                    ln["stream"].cuda_stream), "shiftable_bf")
+                metas_h[i].copy_(m, non_blocking=True)
+        for ln in lane:
+            main.wait_stream(ln["stream"])
+        main.synchronize()
+    tails = metas_h.numpy()
+    results = []
+    for i, t in enumerate(imgs):
+        tail = tails[i]
+        if int(tail[_META_STATS:_META_STATS + 64].view(np.uint64)[7]) != 0:
+            raise InvalidParameterError(f"image {i} contains non-finite samples")
+        plan_c = _lib.SbfPlan.from_buffer_copy(tail[_META_PLAN:_META_PLAN + 64].tobytes())
+        _lib.check(plan_c.status, "plan")
+        if plan_c.flags & (_lib.PLAN_NEEDS_HDR | _lib.PLAN_N_AMBIGUOUS):
+            # rare: wide range or an ambiguous order; the single-image path
+            # resolves both (fp64 re-run / host twin of the plan)
+            r = shiftable_bf(t, params)
+            outs[i].copy_(r.image)
+            results.append(ShiftableResult(outs[i], r.plan, r.fallback_pixels))
+            continue
+        fb = int(tail[_META_FB:_META_FB + 8].view(np.int64)[0])
+        if fb:
+            warnings.warn(f"image {i}: {fb} pixel(s) had a non-positive normalizer; input values kept",
+                          RuntimeWarning, stacklevel=2)
+        results.append(ShiftableResult(outs[i], _plan_from_struct(plan_c), fb))
+    return results
 
 
 def shiftable_bf_poly(img, params: FilterParams) -> ShiftableResult:

@@ -193,6 +193,16 @@ class StripFilter:
                 main.wait_event(e)
         return self.out
 
+    def launches_per_run(self):
+        """Kernels one run() launches: per channel K1 (row + column pass), the
+        plan, and the filter (K3 + epilogue, or two sweeps per term and the
+        epilogue on the split path for radii >= 9)."""
+        n = 0
+        for pl in self.plans_host():
+            K = pl.N // 2 - pl.M + 1
+            n += 3 + (2 * K + 1 if self.sp.r >= 9 else 2)
+        return n
+
     def plans_host(self):
         return [_plan_from_struct(_lib.SbfPlan.from_buffer_copy(self.plans[c].cpu().numpy().tobytes()))
                 for c in range(len(self.bufs))]

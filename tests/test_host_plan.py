@@ -109,3 +109,13 @@ def test_libm_pow_ambiguity_resolved_like_cpython():
     T = 95.65885888902615
     assert O.order_threshold(T, 1.0) == 3706
     assert P.order_threshold(T, 1.0) == 3706        # host twin calls pow() like CPython
+
+
+def test_cfg4_term_table_matches_reference_plans():
+    """workloads.CFG4_K (bench.py's shard weights) == K of the reference's
+    own plans for the 64 config-4 images."""
+    from conftest import golden
+    from paper_1203_5128_b200.workloads import CFG4_K
+    rows = golden("config_plans.npz")["rows"]
+    ks = tuple(int(r[4]) // 2 - int(r[5]) + 1 for r in rows if int(r[0]) == 4)
+    assert ks == CFG4_K
