@@ -40,9 +40,9 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 # our kernels per filtered image (fused pipeline): row max (+ statistics
-# reset), column max (+ accumulator clear, plan in its last CTA), K3 term
-# sweep, K4 epilogue
-KERNELS_PER_IMAGE = 4
+# reset), column max (+ ticket clear, plan in its last CTA), K3 term sweep
+# (+ divide / fallback epilogue)
+KERNELS_PER_IMAGE = 3
 METRIC = "Mpixel/s shiftable Gaussian BF at 1/2/4/8 B200; % of FP32/HBM roofline"
 UNIT = "Mpixel/s"
 OPS_PER_PX_TERM = 132   # phasor 4 + f*c,f*s 2 + 4 images x 6 line passes x 5 + acc 6

@@ -50,6 +50,14 @@ def split_instantiations(kind: str):
     return [(r, 3) for r in range(5, 13)]
 
 
+def sweep_instantiations(kind: str):
+    """(r, passes) pairs with a K3 sweep instantiation (four images per V
+    thread: the 2r+3 register rings of 3 passes fit up to r = 5)."""
+    if kind == "min":
+        return [(2, 3), (4, 3), (5, 3)]
+    return [(r, 3) for r in range(0, 6)] + [(r, 1) for r in range(1, 6)]
+
+
 def _newer(target, deps):
     if not os.path.exists(target):
         return False
@@ -96,8 +104,18 @@ def build(kind: str = "full", jobs: int | None = None, verbose: bool = False,
     if not os.path.exists(sinc) or open(sinc).read() != stext:
         with open(sinc, "w") as fh:
             fh.write(stext)
+    winst = sweep_instantiations(kind)
+    winc = os.path.join(CSRC, "sbf_sweep_list.inc")
+    wtext = "".join(f"SBF_Z({r}, {p})\n" for r, p in winst)
+    if not os.path.exists(winc) or open(winc).read() != wtext:
+        with open(winc, "w") as fh:
+            fh.write(wtext)
     jobs_list = [(os.path.join(CSRC, s), os.path.join(obj_dir, s.replace(".cu", ".o")), defs)
                  for s in SOURCES]
+    for r, p in winst:
+        jobs_list.append((os.path.join(CSRC, "sbf_sweep_inst.cu"),
+                          os.path.join(obj_dir, f"sweep_r{r}_p{p}.o"),
+                          defs + [f"-DSBF_R={r}", f"-DSBF_P={p}"]))
     for r, p in sinst:
         jobs_list.append((os.path.join(CSRC, "sbf_split_inst.cu"),
                           os.path.join(obj_dir, f"split_r{r}_p{p}.o"),

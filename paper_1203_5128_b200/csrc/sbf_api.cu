@@ -13,7 +13,10 @@
 #include "sbf_plan_logic.cuh"
 #include "sbf_generic.h"
 #include "sbf_split.cuh"
+#include "sbf_sweep.cuh"
 #include "sbf_terms.cuh"
+
+#include <cudaTypedefs.h>
 
 namespace sbf {
 
@@ -52,6 +55,30 @@ static const SplitEntry* find_split(const sbf_spatial& sp, int precision) {
   if (sp.r < g_split_min_r || !(sp.alpha <= 0.999)) return nullptr;
   for (const auto& e : reg)
     if (e.r == sp.r && e.passes == sp.passes) return &e;
+  return nullptr;
+}
+
+// ---- registry of K3 sweep instantiations (generated list) ----
+#define SBF_Z(R, P) SweepEntry sweep_entry_##R##_##P();
+#include "sbf_sweep_list.inc"
+#undef SBF_Z
+
+// K3 sweep (TMA-fed, deterministic, fused epilogue): 0 disables it
+static thread_local int g_sweep_on = 1;
+
+static const SweepEntry* find_sweep(const sbf_spatial& sp, int precision) {
+  static const std::vector<SweepEntry> reg = {
+#define SBF_Z(R, P) sweep_entry_##R##_##P(),
+#include "sbf_sweep_list.inc"
+#undef SBF_Z
+  };
+  if (!g_sweep_on || (precision != SBF_PREC_FP32 && precision != SBF_PREC_AUTO)) return nullptr;
+  const int passes = sp.mode == SBF_SPATIAL_BOX ? 1 : sp.passes;
+  const bool box_like = sp.mode == SBF_SPATIAL_BOX || sp.alpha == 0.0;
+  if (sp.mode != SBF_SPATIAL_BOX && sp.mode != SBF_SPATIAL_ITERATED) return nullptr;
+  (void)box_like;
+  for (const auto& e : reg)
+    if (e.r == sp.r && e.passes == passes) return &e;
   return nullptr;
 }
 
@@ -167,6 +194,23 @@ static bool spatial_coeffs(const sbf_spatial& sp, int* r, int* passes, double* a
 // counter per output segment (at most one per row)]
 static size_t terms_ctrl_bytes(int64_t rows_out) { return align_up((size_t)(rows_out + 16) * 4); }
 
+// K3 sweep workspace: [control 256 B | tickets (rows x strips) | (num, den)
+// accumulator | fp32 copy of the input when it is float64 or not TMA-aligned]
+// — the first two are cleared before the launch (by K1 in the fused entry)
+static int64_t sweep_strips(const SweepEntry& w, int64_t W) {
+  int halo, wc, threads, bps;
+  w.geom(&halo, &wc, &threads, &bps);
+  return (W + wc - 1) / wc;
+}
+static size_t sweep_zero_bytes(const SweepEntry& w, int64_t W, int64_t rows_out) {
+  return 256 + align_up((size_t)(rows_out * sweep_strips(w, W)) * 4);
+}
+static size_t sweep_ws(const SweepEntry& w, int64_t H, int64_t W, int64_t rows_out) {
+  const int64_t ldp = (W + 3) / 4 * 4;
+  return sweep_zero_bytes(w, W, rows_out) + align_up((size_t)(rows_out * W) * 8) +
+         align_up((size_t)(H * ldp) * 4);
+}
+
 // partial accumulators (+ an fp32 centred copy of float64 inputs for K3)
 size_t filter_ws(int64_t H, int64_t W, int64_t rows_out, int dtype, const sbf_spatial* sp,
                  int precision) {
@@ -179,6 +223,7 @@ size_t filter_ws(int64_t H, int64_t W, int64_t rows_out, int dtype, const sbf_sp
     if (dtype == SBF_F64) bytes += align_up((size_t)(H * W) * 4);
     return bytes;
   }
+  if (const SweepEntry* w = find_sweep(*sp, precision)) return sweep_ws(*w, H, W, rows_out);
   const TermsEntry* e = find_entry(*sp, precision);
   if (!e) return align_up((size_t)(rows_out * W) * 16);  // generic: one fp64 accumulator
   TermGeom g;
@@ -482,11 +527,122 @@ static int launch_split_path(const FilterLaunch& a, const SplitEntry& se, int r,
   return launch_epilogue<float>(a, reinterpret_cast<const float*>(p.nd), 1, rows_out * a.W);
 }
 
+// ---- K3 sweep path ----
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// fp32 copy for the TMA view: (f - centre) for float64 inputs, f itself for
+// float32 inputs whose row pitch / base are not 16-byte aligned
+__global__ void tma_copy_kernel(const void* __restrict__ f, int dtype, int64_t H, int64_t W,
+                                int64_t ld, const double* __restrict__ stats, float* __restrict__ out,
+                                int64_t ldo) {
+  pdl_wait();
+  const double c = stats[3];
+  for (int64_t y = blockIdx.y; y < H; y += gridDim.y)
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < ldo;
+         x += (int64_t)gridDim.x * blockDim.x) {
+      float v = 0.f;
+      if (x < W)
+        v = dtype == SBF_F64 ? (float)(static_cast<const double*>(f)[y * ld + x] - c)
+                             : static_cast<const float*>(f)[y * ld + x];
+      out[y * ldo + x] = v;
+    }
+}
+
+static int launch_sweep_path(const FilterLaunch& a, const SweepEntry& w, int r, double alpha) {
+  const int64_t rows_out = a.out_hi - a.out_lo;
+  const size_t need = sweep_ws(w, a.H, a.W, rows_out);
+  SBF_REQUIRE(a.ws && a.ws_bytes >= need, SBF_ERR_WORKSPACE,
+              "filter workspace too small (%zu < %zu)", a.ws_bytes, need);
+  auto enc = tensor_map_encoder();
+  SBF_REQUIRE(enc != nullptr, SBF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  char* ws = static_cast<char*>(a.ws);
+  const size_t zb = sweep_zero_bytes(w, a.W, rows_out);
+  const size_t acc_b = align_up((size_t)(rows_out * a.W) * 8);
+  SweepParams p;
+  memset(&p, 0, sizeof(p));
+  p.ctrl = reinterpret_cast<int*>(ws);
+  p.tick = reinterpret_cast<int*>(ws + 256);
+  p.acc = reinterpret_cast<float2*>(ws + zb);
+  const bool direct = a.dtype == SBF_F32 && (a.ld % 4) == 0 &&
+                      (reinterpret_cast<uintptr_t>(a.f) % 16) == 0;
+  if (direct) {
+    p.f = static_cast<const float*>(a.f);
+    p.ld = a.ld;
+    p.centred = 0;
+  } else {
+    float* fc = reinterpret_cast<float*>(ws + zb + acc_b);
+    const int64_t ldo = (a.W + 3) / 4 * 4;
+    const dim3 grid((unsigned)smin<int64_t>((ldo + 255) / 256, 64),
+                    (unsigned)smin<int64_t>(a.H, 65535));
+    SBF_CHECK_CUDA(launch_pdl(tma_copy_kernel, grid, dim3(256), 0, a.stream, a.f, a.dtype, a.H, a.W,
+                              a.ld, a.stats, fc, ldo));
+    p.f = fc;
+    p.ld = ldo;
+    p.centred = a.dtype == SBF_F64 ? 1 : 0;
+  }
+  if ((g_stage_mask & 1) && !a.nd_zeroed) SBF_CHECK_CUDA(cudaMemsetAsync(ws, 0, zb, a.stream));
+  p.fo = a.f;
+  p.fo_ld = a.ld;
+  p.fo_dtype = a.dtype;
+  p.out = a.out;
+  p.out_dtype = a.out_dtype;
+  p.H = (int)a.H;
+  p.W = (int)a.W;
+  p.row0 = a.row0;
+  p.img_H = a.img_H;
+  p.out_lo = (int)a.out_lo;
+  p.out_hi = (int)a.out_hi;
+  p.band = (int)smin<int64_t>(rows_out, 512);
+  p.nstrips = (int)sweep_strips(w, a.W);
+  p.r = r;
+  p.alpha = (float)alpha;
+  const double cint = 2.0 * r + 1.0 + 2.0 * alpha;
+  p.a = (float)((1.0 - alpha) / cint);
+  p.b = (float)(alpha / cint);
+  p.plan = a.plan;
+  p.terms = a.terms;
+  p.stats = a.stats;
+  p.fallback = a.fallback;
+  p.hdr_guard = g_hdr_guard;
+  // TMA view of the fp32 image: 128 columns x `rows` rows per box,
+  // zero-filled outside the buffer
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)a.W, (cuuint64_t)a.H};
+  cuuint64_t strides[1] = {(cuuint64_t)p.ld * 4};
+  cuuint32_t box[2] = {132u, (cuuint32_t)w.rows};  // SweepCfg::FCOLS
+  cuuint32_t es[2] = {1u, 1u};
+  const CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(p.f), dims,
+                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SBF_REQUIRE(cr == CUDA_SUCCESS, SBF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  if (!(g_stage_mask & 1)) return SBF_OK;
+  if (g_k3_ev[0]) SBF_CHECK_CUDA(cudaEventRecord(g_k3_ev[0], a.stream));
+  int rc = w.launch(map, p, a.stream);
+  if (rc != SBF_OK) return rc;
+  if (g_k3_ev[1]) SBF_CHECK_CUDA(cudaEventRecord(g_k3_ev[1], a.stream));
+  return SBF_OK;
+}
+
 size_t k3_zero_bytes(const FilterLaunch& a) {
   int r, passes;
   double alpha;
   if (!spatial_coeffs(a.sp, &r, &passes, &alpha)) return 0;
   if (a.precision != SBF_PREC_FP32 && a.precision != SBF_PREC_AUTO) return 0;
+  if (!find_split(a.sp, SBF_PREC_FP32))
+    if (const SweepEntry* w = find_sweep(a.sp, SBF_PREC_FP32))
+      return g_stage_mask == 3 ? sweep_zero_bytes(*w, a.W, a.out_hi - a.out_lo) : 0;
   if (!find_entry(a.sp, SBF_PREC_FP32) || find_split(a.sp, SBF_PREC_FP32)) return 0;
   if (g_stage_mask != 3) return 0;
   const int64_t rows_out = a.out_hi - a.out_lo;
@@ -514,7 +670,7 @@ int launch_filter(const FilterLaunch& a) {
     FilterLaunch b = a;
     b.precision = SBF_PREC_FP32;
     const TermsEntry* e3 = find_entry(b.sp, SBF_PREC_FP32);
-    if (!e3 || find_split(b.sp, SBF_PREC_FP32)) {
+    if ((!e3 && !find_sweep(b.sp, SBF_PREC_FP32)) || find_split(b.sp, SBF_PREC_FP32)) {
       double st[8];
       SBF_CHECK_CUDA(cudaMemcpyAsync(st, a.stats, sizeof(st), cudaMemcpyDeviceToHost, a.stream));
       SBF_CHECK_CUDA(cudaStreamSynchronize(a.stream));
@@ -535,6 +691,7 @@ int launch_filter(const FilterLaunch& a) {
   SBF_REQUIRE(a.H <= INT32_MAX && a.W <= INT32_MAX, SBF_ERR_INVALID, "image too large");
 
   if (const SplitEntry* se = find_split(a.sp, a.precision)) return launch_split_path(a, *se, r, alpha);
+  if (const SweepEntry* w = find_sweep(a.sp, a.precision)) return launch_sweep_path(a, *w, r, alpha);
   const TermsEntry* e = find_entry(a.sp, a.precision);
   if (!e) {
     const size_t need = align_up((size_t)(rows_out * a.W) * 16);
