@@ -64,7 +64,10 @@ static const SplitEntry* find_split(const sbf_spatial& sp, int precision) {
 #undef SBF_Z
 
 // K3 sweep (TMA-fed, deterministic, fused epilogue): 0 disables it
-static thread_local int g_sweep_on = 1;
+#ifndef SBF_SWEEP_ON
+#define SBF_SWEEP_ON 1
+#endif
+static thread_local int g_sweep_on = SBF_SWEEP_ON;
 
 static const SweepEntry* find_sweep(const sbf_spatial& sp, int precision) {
   static const std::vector<SweepEntry> reg = {
@@ -194,21 +197,24 @@ static bool spatial_coeffs(const sbf_spatial& sp, int* r, int* passes, double* a
 // counter per output segment (at most one per row)]
 static size_t terms_ctrl_bytes(int64_t rows_out) { return align_up((size_t)(rows_out + 16) * 4); }
 
-// K3 sweep workspace: [control 256 B | tickets (rows x strips) | (num, den)
-// accumulator | fp32 copy of the input when it is float64 or not TMA-aligned]
-// — the first two are cleared before the launch (by K1 in the fused entry)
+// K3 sweep workspace: [control 256 B | segment counters (32-row segments x
+// strips) | fixed-point accumulator (8 B/px) | fp32 copy of the input when it
+// is float64 or not TMA-aligned] — the first three are cleared before the
+// launch (by K1 in the fused entry)
 static int64_t sweep_strips(const SweepEntry& w, int64_t W) {
   int halo, wc, threads, bps;
   w.geom(&halo, &wc, &threads, &bps);
   return (W + wc - 1) / wc;
 }
+static size_t sweep_seg_bytes(const SweepEntry& w, int64_t W, int64_t rows_out) {
+  return align_up((size_t)(((rows_out + 31) / 32) * sweep_strips(w, W)) * 4);
+}
 static size_t sweep_zero_bytes(const SweepEntry& w, int64_t W, int64_t rows_out) {
-  return 256 + align_up((size_t)(rows_out * sweep_strips(w, W)) * 4);
+  return 256 + sweep_seg_bytes(w, W, rows_out) + align_up((size_t)(rows_out * W) * 8);
 }
 static size_t sweep_ws(const SweepEntry& w, int64_t H, int64_t W, int64_t rows_out) {
   const int64_t ldp = (W + 3) / 4 * 4;
-  return sweep_zero_bytes(w, W, rows_out) + align_up((size_t)(rows_out * W) * 8) +
-         align_up((size_t)(H * ldp) * 4);
+  return sweep_zero_bytes(w, W, rows_out) + align_up((size_t)(H * ldp) * 4);
 }
 
 // partial accumulators (+ an fp32 centred copy of float64 inputs for K3)
@@ -568,12 +574,11 @@ static int launch_sweep_path(const FilterLaunch& a, const SweepEntry& w, int r, 
   SBF_REQUIRE(enc != nullptr, SBF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   char* ws = static_cast<char*>(a.ws);
   const size_t zb = sweep_zero_bytes(w, a.W, rows_out);
-  const size_t acc_b = align_up((size_t)(rows_out * a.W) * 8);
   SweepParams p;
   memset(&p, 0, sizeof(p));
   p.ctrl = reinterpret_cast<int*>(ws);
-  p.tick = reinterpret_cast<int*>(ws + 256);
-  p.acc = reinterpret_cast<float2*>(ws + zb);
+  p.seg = reinterpret_cast<int*>(ws + 256);
+  p.acc = reinterpret_cast<unsigned long long*>(ws + 256 + sweep_seg_bytes(w, a.W, rows_out));
   const bool direct = a.dtype == SBF_F32 && (a.ld % 4) == 0 &&
                       (reinterpret_cast<uintptr_t>(a.f) % 16) == 0;
   if (direct) {
@@ -581,7 +586,7 @@ static int launch_sweep_path(const FilterLaunch& a, const SweepEntry& w, int r, 
     p.ld = a.ld;
     p.centred = 0;
   } else {
-    float* fc = reinterpret_cast<float*>(ws + zb + acc_b);
+    float* fc = reinterpret_cast<float*>(ws + zb);
     const int64_t ldo = (a.W + 3) / 4 * 4;
     const dim3 grid((unsigned)smin<int64_t>((ldo + 255) / 256, 64),
                     (unsigned)smin<int64_t>(a.H, 65535));

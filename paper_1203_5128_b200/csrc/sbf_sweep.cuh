@@ -67,8 +67,8 @@ struct SweepParams {
   int band;
   int nstrips;
   int* ctrl;    // [0] work-queue head (zeroed before launch)
-  int* tick;    // per (output row, strip): terms accumulated (zeroed before launch)
-  float2* acc;  // (num, den) per output pixel, rows [out_lo, out_hi)
+  int* seg;     // per (32-row output segment, strip): items landed (zeroed before launch)
+  unsigned long long* acc;  // fixed-point (num | den) per output pixel (zeroed before launch)
   int r;
   float alpha;
   float a, b;
@@ -89,17 +89,16 @@ struct SweepCfg {
   // the strip's first column rounded down to a multiple of 4
   static constexpr int FCOLS = COLS + 4;
   static constexpr int WC = COLS - 2 * HALO;       // output columns per strip
-  static constexpr int CH = 32 / L;                // blocks per chunk
-  static constexpr int ROWS = CH * L;              // stream steps (VB rows) per chunk
-  static constexpr int NB = (COLS + L - 1) / L;    // H-phase blocks per row
+  static constexpr int ROWS = COLS / 4;            // stream steps (VB rows) per chunk: one H lane per (row, image)
+  static constexpr int NB = (COLS + L) / L;        // H-phase blocks per row (>= COLS + 1 steps)
   static constexpr int VB_COLS = NB * L;
   static constexpr int VB_PITCH = 4 * VB_COLS + 4;  // floats; == 4 mod 32 words for 8 rows
   static constexpr int RING = ((ROWS + HALO + L - 1) / L) * L;  // phasor ring (steps)
-  static constexpr int RAW_PITCH = 2 * WC + 2;
+  static constexpr int RAW_PITCH = WC + 1;
   static constexpr int GOFF = (PASSES + 2) * D + 2;
   static constexpr int THREADS = COLS;
-  static_assert(WC > 0 && CH >= 1, "halo too wide for a 128-column strip");
-  static_assert(ROWS * 4 <= THREADS + 32, "H phase: one (row, image) lane per thread");
+  static constexpr int SEGR = 32;  // output rows per epilogue segment
+  static_assert(WC > 0, "halo too wide for a 128-column strip");
   static constexpr size_t F_BYTES = (size_t)ROWS * FCOLS * 4;
   static constexpr size_t VB_BYTES = (size_t)ROWS * VB_PITCH * 4;
   static constexpr size_t RAW_BYTES = (size_t)RING * RAW_PITCH * 4;
@@ -270,9 +269,9 @@ template <int R, int PASSES>
 __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
     sweep_kernel(const __grid_constant__ CUtensorMap fmap, const SweepParams p) {
   using C = SweepCfg<R, PASSES>;
-  constexpr int D = C::D, L = C::L, HALO = C::HALO, WC = C::WC, COLS = C::COLS, CH = C::CH;
+  constexpr int D = C::D, L = C::L, HALO = C::HALO, WC = C::WC, COLS = C::COLS;
   constexpr int ROWS = C::ROWS, VBP = C::VB_PITCH, RING = C::RING, RAWP = C::RAW_PITCH;
-  constexpr int GOFF = C::GOFF, NB = C::NB, THREADS = C::THREADS;
+  constexpr int GOFF = C::GOFF, NB = C::NB, THREADS = C::THREADS, SEGR = C::SEGR;
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // the TMA destination must be 128-byte aligned in the shared window: the
@@ -280,11 +279,13 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
   unsigned char* sbase = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   uint64_t& s_bar = *reinterpret_cast<uint64_t*>(sbase);
   int& s_item = *reinterpret_cast<int*>(sbase + 8);
+  int& s_ndone = *reinterpret_cast<int*>(sbase + 12);
+  int* s_done = reinterpret_cast<int*>(sbase + 16);  // <= 28 segments per item
   float* FT = reinterpret_cast<float*>(sbase + 128);  // TMA box: ROWS x FCOLS
   float* VB = FT + ROWS * C::FCOLS;
   float* RAW = VB + ROWS * VBP;
   float* gv = RAW + RING * RAWP;
-  const int gv_len = p.band + 2 * HALO + GOFF + CH * L;
+  const int gv_len = p.band + 2 * HALO + GOFF + ROWS;
   float* gh = gv + gv_len;
 
   pdl_wait();  // K1 / K2 results (programmatic dependent launch)
@@ -301,6 +302,12 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
   const float centerf = (float)p.stats[3];
   const float fcent = p.centred ? 0.f : centerf;  // the fp32 view may be centred already
   const double centerd = p.stats[3];
+  // fixed-point scales: |den| <= sum of the term weights <= 1 + tiny, and
+  // |num| <= max|f - centre| times the same (|S[z]| <= 1 for an averaging S)
+  const double maxdev = fmax(p.stats[2] - centerd, centerd - p.stats[1]);
+  const int nexp = ilogb(fmax(maxdev, 1.0)) + 1;  // maxdev < 2^nexp
+  const float nscale = ldexpf(1.f, 29 - nexp), dscale = ldexpf(1.f, 29);
+  const double inv_nscale = ldexp(1.0, nexp - 29), inv_dscale = ldexp(1.0, -29);
   if (K_eval <= 0) {
     // no retained term: every normaliser is 0, so every pixel falls back
     unsigned long long n = 0;
@@ -374,13 +381,11 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
     const int y1 = min(p.out_hi, y0 + bh);
     const int Bn = y1 - y0;
     const int T_total = Bn + 2 * HALO;
-    const int nblk = (T_total + L - 1) / L;
-    const int nchunks = (nblk + CH - 1) / CH;
+    const int nchunks = (T_total + ROWS - 1) / ROWS;
     const int xs = strip * WC - HALO;  // image column of haloed index 0
     const int xa = xs & ~3;             // box start (16-byte aligned column)
     const int xoff = xs - xa;
     const int64_t grow0 = p.row0 + (int64_t)(y0 - HALO);  // global row of stream position 0
-    const bool first_term = kk == 0, last_term = kk == K_eval - 1;
 
     // border tables (index = stream / haloed position + GOFF)
     for (int k = tid; k < nchunks * ROWS + GOFF; k += THREADS)
@@ -437,16 +442,22 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
       }
 
       // ===================== V phase =====================
-      auto vblock = [&](auto border_tag, const int blk) {
-        constexpr bool BORDER = decltype(border_tag)::value;
-        const int base = t0 + blk * L;
-        const float* fsrc = FT + blk * L * C::FCOLS + q + xoff;
-        float* vdst = VB + blk * L * VBP + 4 * q;
+      // steps [t0, t0 + ROWS) in blocks of L aligned to the stream position
+      // (the ring slot of step t is t mod L): interior blocks wholly inside
+      // the chunk run without checks, blocks cut by a chunk boundary check
+      // the step range, blocks near the image's top or bottom renormalise
+      auto vblock = [&](auto kind_tag, const int base) {
+        constexpr int KIND = decltype(kind_tag)::value;  // 0 fast, 1 partial, 2 border
+        constexpr bool BORDER = KIND == 2;
+        const int rel = base - t0;  // chunk row of step base (may be < 0)
+        const float* fsrc = FT + rel * C::FCOLS + q + xoff;
+        float* vdst = VB + rel * VBP + 4 * q;
         const int rs0 = base % RING;
-        float* rdst = RAW + rs0 * RAWP + 2 * (q - HALO);
+        float* rdst = RAW + rs0 * RAWP + (q - HALO);
         const bool out_col = q >= HALO && q < HALO + WC;
         sweep_for<L>([&](auto jc) {
           constexpr int J = decltype(jc)::value;
+          if (KIND != 0 && (unsigned)(rel + J) >= (unsigned)ROWS) return;
           const float fc = fsrc[J * C::FCOLS] - fcent;
           float sv, cv;
           __sincosf(fc * omega, &sv, &cv);
@@ -456,7 +467,8 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
             cv *= m;
             sv *= m;
           }
-          if (out_col) sts2(rdst + J * RAWP, make_float2(cv, sv));
+          // the output pixel's sample, for its phasor in the accumulate phase
+          if (out_col) rdst[J * RAWP] = fc;
           const float* gt = gv + base + J + GOFF;
           const float2 fx = make_float2(fc, 1.f);
           const float2 ya = vcascade<J, L, D, PASSES, BORDER>(dA, lA, __fmul2_rn(fx, pk(cv)), a2, nb2, b2, gt);
@@ -467,14 +479,14 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
         });
       };
 #pragma unroll 1
-      for (int blk = 0; blk < CH; ++blk) {
-        const int base = t0 + blk * L;
-        if (base >= nblk * L) break;
+      for (int base = (t0 / L) * L; base < t0 + ROWS; base += L) {
         const bool clean = base - (PASSES + 2) * D - 1 >= sg_lo && base + L - 1 <= sg_hi;
-        if (clean)
-          vblock(std::false_type{}, blk);
+        if (!clean)
+          vblock(std::integral_constant<int, 2>{}, base);
+        else if (base >= t0 && base + L <= t0 + ROWS)
+          vblock(std::integral_constant<int, 0>{}, base);
         else
-          vblock(std::true_type{}, blk);
+          vblock(std::integral_constant<int, 1>{}, base);
       }
       __syncthreads();  // VB complete; the f box is consumed
       // next chunk's box streams in while the H phase runs
@@ -485,6 +497,9 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
       const int vhi = min(t0 + ROWS, 2 * HALO + Bn) - t0;
 
       // ===================== H phase =====================
+      // 4 lanes per row (one per image) stream the chunk's rows; blocks whose
+      // columns all have factor 1 need no renormalisation (every block of an
+      // interior strip; all but the outer blocks of the two edge strips)
       if (hv >= vlo && hv < vhi) {
         float* vrow = VB + hv * VBP + himg;
         float hd[PASSES][L];
@@ -527,106 +542,112 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
           });
         } else {
 #pragma unroll 1
-          for (int kb = 0; kb < NB; ++kb) hblock(std::integral_constant<int, 3>{}, kb * L);
+          for (int kb = 0; kb < NB; ++kb) {
+            const int hb = kb * L;
+            // the block reads factors back to hb - (PASSES+2) D - 1
+            if (hb - (PASSES + 2) * D - 1 >= qg_lo && hb + L - 1 <= qg_hi)
+              hblock(std::integral_constant<int, 2>{}, hb);
+            else
+              hblock(std::integral_constant<int, 3>{}, hb);
+          }
         }
       }
       __syncthreads();
 
-      // ===================== accumulate (+ epilogue) =====================
+      // ===================== accumulate =====================
+      // (num, den) of this term in 32-bit fixed point, both halves of one
+      // 64-bit integer, added with one red.add.u64 per pixel: integer sums
+      // are associative, so the result does not depend on the order in
+      // which items land (bit-reproducible), and nothing waits
       if (vlo < vhi) {
-        // output rows of this chunk (relative to out_lo)
-        const int ra = y0 - 2 * HALO + t0 + vlo - p.out_lo;
+        const int ra = y0 - 2 * HALO + t0 + vlo - p.out_lo;  // first output row (rel. out_lo)
         const int nr = vhi - vlo;
-        int* tk = p.tick + (int64_t)ra * p.nstrips + strip;
-        if (!first_term && tid < nr) {
-          // wait until every earlier term has accumulated these rows
-          int* tp = tk + (int64_t)tid * p.nstrips;
-          while (ld_acquire(tp) != kk) __nanosleep(32);
-        }
-        __syncthreads();
         const int xlim = min(WC, p.W - strip * WC);
         const int jc = tid;
-        unsigned long long bad = 0;
         if (jc < xlim) {
           const int col = strip * WC + jc;
           const float* vb = VB + vlo * VBP + 4 * (HALO + jc);
-          float2* dst = p.acc + (int64_t)ra * p.W + col;
-          // output row y0 - 2 HALO + t0 + v has its phasor at step t0 + v - HALO
-          const int slot0 = (t0 + vlo - HALO) % RING;
-          const float* rp = RAW + 2 * jc;
-          // the chunk's rows in batches: all accumulator loads of a batch are
-          // in flight together (one L2 round trip per batch)
-          constexpr int NBT = R >= 5 ? 5 : 8;
-#pragma unroll 1
-          for (int v0 = 0; v0 < nr; v0 += NBT) {
-            float2 nd[NBT];
-            float2 prev[NBT];
-#pragma unroll
-            for (int u = 0; u < NBT; ++u)
-              if (!first_term && v0 + u < nr) prev[u] = __ldcg(dst + (int64_t)(v0 + u) * p.W);
-#pragma unroll
-            for (int u = 0; u < NBT; ++u) {
-              if (v0 + u < nr) {
-                const int v = v0 + u;
-                int slot = slot0 + v;
-                slot = slot >= RING ? slot - RING : slot;
-                const float4 pv = *reinterpret_cast<const float4*>(vb + v * VBP);
-                const float2 ph = *reinterpret_cast<const float2*>(rp + slot * RAWP);
-                float2 t = __ffma2_rn(pk(ph.y), make_float2(pv.z, pv.w),
-                                      __fmul2_rn(pk(ph.x), make_float2(pv.x, pv.y)));
-                t = __fmul2_rn(t, pk(scale));
-                nd[u] = first_term ? t : __fadd2_rn(t, prev[u]);
-              }
-            }
-            if (!last_term) {
-#pragma unroll
-              for (int u = 0; u < NBT; ++u)
-                if (v0 + u < nr) __stcg(dst + (int64_t)(v0 + u) * p.W, nd[u]);
-            } else {
-#pragma unroll
-              for (int u = 0; u < NBT; ++u) {
-                if (v0 + u >= nr) break;
-                const int v = v0 + u;
-                const int64_t orow = p.out_lo + ra + v;
-                const int64_t oi = (int64_t)(ra + v) * p.W + col;
-                const float2 t = nd[u];
-                const bool is_bad = !(t.y > 0.f);  // bilateral.py:244 (NaN counts as bad)
-                bad += is_bad ? 1 : 0;
-                if (p.out_dtype == SBF_F32) {
-                  float o;
-                  if (is_bad)
-                    o = p.fo_dtype == SBF_F32 ? static_cast<const float*>(p.fo)[orow * p.fo_ld + col]
-                                              : (float)static_cast<const double*>(p.fo)[orow * p.fo_ld + col];
-                  else
-                    o = t.x / t.y + centerf;
-                  static_cast<float*>(p.out)[oi] = o;
-                } else {
-                  double o;
-                  if (is_bad)
-                    o = p.fo_dtype == SBF_F32 ? (double)static_cast<const float*>(p.fo)[orow * p.fo_ld + col]
-                                              : static_cast<const double*>(p.fo)[orow * p.fo_ld + col];
-                  else
-                    o = (double)t.x / (double)t.y + centerd;
-                  static_cast<double*>(p.out)[oi] = o;
-                }
-              }
-            }
+          unsigned long long* dst = p.acc + (int64_t)ra * p.W + col;
+          // output row y0 - 2 HALO + t0 + v was sampled at step t0 + v - HALO;
+          // its phasor is recomputed from the sample exactly as the V phase did
+          int slot = (t0 + vlo - HALO) % RING;
+          const float* rp = RAW + jc;
+          const float2 fx = make_float2(scale * nscale, scale * dscale);
+#pragma unroll 4
+          for (int v = 0; v < nr; ++v) {
+            const float4 pv = *reinterpret_cast<const float4*>(vb + v * VBP);
+            const float fcv = rp[slot * RAWP];
+            slot = slot + 1 == RING ? 0 : slot + 1;
+            float sv, cv;
+            __sincosf(fcv * omega, &sv, &cv);
+            float2 t = __ffma2_rn(pk(sv), make_float2(pv.z, pv.w),
+                                  __fmul2_rn(pk(cv), make_float2(pv.x, pv.y)));
+            t = __fmul2_rn(t, fx);
+            const long long q = ((long long)__float2int_rn(t.x) << 32) + (long long)__float2int_rn(t.y);
+            asm volatile("red.global.add.u64 [%0], %1;" ::"l"(dst + (int64_t)v * p.W), "l"(q) : "memory");
           }
         }
-        if (last_term) {
-          for (int o = 16; o; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
-          if ((tid & 31) == 0 && bad) atomicAdd(p.fallback, bad);
-        }
-        __syncthreads();  // every column of these rows has landed
-        if (!last_term && tid < nr) st_release(tk + (int64_t)tid * p.nstrips, kk + 1);
       }
-      if (!SBF_SWEEP_TMA && c + 1 < nchunks) {
-        __syncthreads();  // every thread's V reads of the box are done
-        load_box(fbuf_row0 + t0 + ROWS);
-        __syncthreads();
-      }
+      __syncthreads();  // VB / RAW are rewritten by the next chunk
     }  // chunks
-    __syncthreads();  // tables and VB are rewritten by the next item
+    // this item's rows are in: count it on the output segments it covers;
+    // the item that completes a segment (all terms, all bands over it)
+    // divides it out (bilateral.py:242-254) and writes the output
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      int n = 0;
+      const int s0 = (y0 - p.out_lo) / SEGR, s1 = (y1 - 1 - p.out_lo) / SEGR;
+      for (int sg = s0; sg <= s1; ++sg) {
+        const int r0 = sg * SEGR, r1 = min(rows_all, r0 + SEGR) - 1;
+        const int nm = r1 / bandh - r0 / bandh + 1;
+        const int nt = Ks > 0 ? r1 / bandh_s - r0 / bandh_s + 1 : 0;
+        const int expected = (K_eval - Ks) * nm + Ks * nt;
+        if (atomicAdd(p.seg + (int64_t)sg * p.nstrips + strip, 1) == expected - 1) s_done[n++] = sg;
+      }
+      s_ndone = n;
+      __threadfence();
+    }
+    __syncthreads();
+    const int ndone = s_ndone;
+    if (ndone > 0) {
+      const int xlim = min(WC, p.W - strip * WC);
+      unsigned long long bad = 0;
+      for (int d = 0; d < ndone; ++d) {
+        const int r0 = s_done[d] * SEGR, r1 = min(rows_all, r0 + SEGR);
+        for (int i = tid; i < (r1 - r0) * xlim; i += THREADS) {
+          const int rr = r0 + i / xlim, col = strip * WC + i % xlim;
+          const int64_t ai = (int64_t)rr * p.W + col;
+          const long long sum = (long long)__ldcg(p.acc + ai);
+          const int lo = (int)(unsigned)(sum & 0xffffffffll);
+          const long long hi = (sum - (long long)lo) >> 32;
+          const double num = (double)hi * inv_nscale, den = (double)lo * inv_dscale;
+          const bool is_bad = !(den > 0.0);  // bilateral.py:244 (NaN counts as bad)
+          bad += is_bad ? 1 : 0;
+          const int64_t fi = (int64_t)(p.out_lo + rr) * p.fo_ld + col;
+          if (p.out_dtype == SBF_F32) {
+            float o;
+            if (is_bad)
+              o = p.fo_dtype == SBF_F32 ? static_cast<const float*>(p.fo)[fi]
+                                        : (float)static_cast<const double*>(p.fo)[fi];
+            else
+              o = (float)(num / den) + centerf;
+            static_cast<float*>(p.out)[ai] = o;
+          } else {
+            double o;
+            if (is_bad)
+              o = p.fo_dtype == SBF_F32 ? (double)static_cast<const float*>(p.fo)[fi]
+                                        : static_cast<const double*>(p.fo)[fi];
+            else
+              o = num / den + centerd;
+            static_cast<double*>(p.out)[ai] = o;
+          }
+        }
+      }
+      for (int o = 16; o; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+      if ((tid & 31) == 0 && bad) atomicAdd(p.fallback, bad);
+    }
+    __syncthreads();  // tables, VB and the segment list are rewritten by the next item
   }  // work queue
 }
 
@@ -635,7 +656,7 @@ template <int R, int PASSES>
 size_t sweep_smem_bytes(int band) {
   using C = SweepCfg<R, PASSES>;
   return 256 + C::F_BYTES + C::VB_BYTES + C::RAW_BYTES +
-         (size_t)(band + 2 * C::HALO + C::GOFF + C::CH * C::L + C::ROWS + C::COLS + C::GOFF) * 4 + 16;
+         (size_t)(band + 2 * C::HALO + C::GOFF + C::ROWS + C::COLS + C::GOFF) * 4 + 16;
 }
 
 template <int R, int PASSES>
