@@ -121,6 +121,15 @@ int sbf_support_radius(const sbf_spatial* sp, int* radius);
 int sbf_truncation_index_exact(int N, double epsilon, int* M);
 int sbf_truncation_index_chernoff(int N, double epsilon, double log_2_over_eps, int* M);
 int sbf_order_threshold(double T, double sigma_r, int* N);
+/* C(N, n) / 2^N for n in [lo, hi], correctly rounded to float64 (exact
+ * multi-limb integers on the host) — replaces kernels.py:198-212
+ * binomial_weights; raised_cosine_expansion builds on it. */
+int sbf_binomial_weights(int N, int lo, int hi, double* out);
+/* Brute-force local range (maxfilter.py:64-82 brute_force_T): O(R^2) per
+ * pixel on the device, independent of the separable max filter; the result
+ * is written to *T_out (host) after a stream synchronisation. */
+int sbf_brute_force_T(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int R,
+                      double* T_out, void* stream);
 int sbf_select_plan(double T, double sigma_r, double epsilon, int rule,
                     double log_2_over_eps, sbf_plan* out);
 

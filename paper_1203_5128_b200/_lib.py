@@ -58,6 +58,8 @@ _SIGS = {
     "sbf_truncation_index_exact": (_int, [_int, _dbl, C.POINTER(_int)]),
     "sbf_truncation_index_exact_bigint": (_int, [_int, _dbl, C.POINTER(_int)]),
     "sbf_truncation_index_chernoff": (_int, [_int, _dbl, _dbl, C.POINTER(_int)]),
+    "sbf_binomial_weights": (_int, [_int, _int, _int, _vp]),
+    "sbf_brute_force_T": (_int, [_vp, _int, _i64, _i64, _i64, _int, C.POINTER(_dbl), _vp]),
     "sbf_select_plan": (_int, [_dbl, _dbl, _dbl, _int, _dbl, C.POINTER(SbfPlan)]),
     "sbf_local_range_workspace": (C.c_size_t, [_i64, _i64, _int]),
     "sbf_local_range": (_int, [_vp, _int, _i64, _i64, _i64, _int, _i64, _i64, _vp, _vp, _vp,

@@ -13,6 +13,8 @@
 // neighbours contribute (the reference's offset_slices), num / den in fp32,
 // den <= 0 (impossible with the positive Gaussian) falls back to the input.
 // Wide-range (HDR) images run an fp64 twin with the reference's arithmetic.
+#include <string.h>
+
 #include "sbf_common.cuh"
 
 namespace sbf {
@@ -266,5 +268,67 @@ extern "C" int sbf_direct_bf_expansion(const void* f, int dtype, int64_t H, int6
 #undef SBF_DT
   SBF_CHECK_LAUNCH();
   // the pageable source was staged by cudaMemcpyAsync before it returned
+  return SBF_OK;
+}
+
+// Brute-force local range (reference maxfilter.py:64-82 `brute_force_T`):
+// max over every pixel x and every offset y with |y|_inf <= R inside the image
+// of |f(x+y) - f(x)|, in float64.  O(R^2) per pixel and independent of K1's
+// separable max filter, so it cross-checks compute_T (the paper's
+// Proposition 1 says both are equal).  One thread per pixel, block maximum,
+// one 64-bit atomicMax of the order-preserving bit image per block.
+namespace sbf {
+template <typename T>
+__global__ void brute_T_kernel(const T* __restrict__ f, int64_t H, int64_t W, int64_t ld, int R,
+                               unsigned long long* __restrict__ best) {
+  __shared__ unsigned long long s_best[8];
+  double m = 0.0;
+  const int64_t n = H * W;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t y = i / W, x = i - y * W;
+    const double c = (double)f[y * ld + x];
+    const int64_t y0 = y - R < 0 ? 0 : y - R, y1 = y + R >= H ? H - 1 : y + R;
+    const int64_t x0 = x - R < 0 ? 0 : x - R, x1 = x + R >= W ? W - 1 : x + R;
+    for (int64_t yy = y0; yy <= y1; ++yy)
+      for (int64_t xx = x0; xx <= x1; ++xx) m = fmax(m, fabs((double)f[yy * ld + xx] - c));
+  }
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) s_best[threadIdx.x >> 5] = ord_bits(m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long b = s_best[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) b = b > s_best[w] ? b : s_best[w];
+    atomicMax(best, b);
+  }
+}
+}  // namespace sbf
+
+extern "C" int sbf_brute_force_T(const void* f, int dtype, int64_t H, int64_t W, int64_t ld, int R,
+                                 double* T_out, void* stream) {
+  using namespace sbf;
+  SBF_REQUIRE(f && T_out && H >= 1 && W >= 1 && ld >= W && R >= 0 &&
+                  (dtype == SBF_F32 || dtype == SBF_F64),
+              SBF_ERR_INVALID, "bad brute_force_T arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DevBuf<unsigned long long> best(st);
+  SBF_CHECK_CUDA(best.alloc(1));
+  const unsigned long long zero = 0x8000000000000000ull;  // ord_bits(+0.0)
+  SBF_CHECK_CUDA(cudaMemcpyAsync(best.p, &zero, sizeof(zero), cudaMemcpyHostToDevice, st));
+  const int threads = 256;
+  const unsigned blocks = (unsigned)smin<int64_t>((H * W + threads - 1) / threads, 148 * 16);
+  if (dtype == SBF_F32)
+    brute_T_kernel<float><<<blocks, threads, 0, st>>>(static_cast<const float*>(f), H, W, ld, R, best.p);
+  else
+    brute_T_kernel<double><<<blocks, threads, 0, st>>>(static_cast<const double*>(f), H, W, ld, R, best.p);
+  SBF_CHECK_LAUNCH();
+  unsigned long long b = 0;
+  SBF_CHECK_CUDA(cudaMemcpyAsync(&b, best.p, sizeof(b), cudaMemcpyDeviceToHost, st));
+  SBF_CHECK_CUDA(cudaStreamSynchronize(st));
+  // ord_value on the host: the maximum is >= +0.0, so the sign bit is set
+  b &= 0x7fffffffffffffffull;
+  double t;
+  memcpy(&t, &b, sizeof(t));
+  *T_out = t;
   return SBF_OK;
 }

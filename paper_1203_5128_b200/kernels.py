@@ -161,42 +161,51 @@ def select_plan(T, sigma_r, epsilon, family=KernelFamily.RAISED_COSINE,
 
 
 def binomial_weights(N, lo, hi) -> np.ndarray:
-    """C(N, n)/2^N for n in [lo, hi], correctly rounded (kernels.py:198-212)."""
-    if not 0 <= lo <= hi <= N:
+    """C(N, n)/2^N for n in [lo, hi], correctly rounded to float64.
+
+    Same contract as reference kernels.py:198-212; computed by the library's
+    host twin (sbf_binomial_weights: exact multi-limb integers, round half to
+    even, subnormals included)."""
+    if not (isinstance(N, (int, np.integer)) and 0 <= lo <= hi <= N):
         raise InvalidParameterError("need 0 <= lo <= hi <= N")
-    denom = 1 << N
-    c = math.comb(N, lo)
-    out = np.empty(hi - lo + 1)
-    for i, n in enumerate(range(lo, hi + 1)):
-        out[i] = c / denom
-        c = c * (N - n) // (n + 1)
+    out = np.empty(int(hi) - int(lo) + 1, dtype=np.float64)
+    _lib.check(_lib.load().sbf_binomial_weights(int(N), int(lo), int(hi), out.ctypes.data),
+               "binomial_weights")
     return out
 
 
 def raised_cosine_expansion(plan: KernelPlan) -> Expansion:
-    """Retained terms n in [M, N-M] of the cosine expansion (kernels.py:215-227)."""
+    """Retained terms n in [M, N-M]: weight C(N,n)/2^N, frequency
+    (2n - N)/(sqrt(N) sigma_r) (reference kernels.py:215-227)."""
     if plan.family is not KernelFamily.RAISED_COSINE:
         raise InvalidParameterError("expansion defined for the raised-cosine family")
-    n = np.arange(plan.M, plan.N - plan.M + 1)
-    weights = binomial_weights(plan.N, plan.M, plan.N - plan.M)
-    freqs = (2 * n - plan.N) / (math.sqrt(plan.N) * plan.sigma_r)
-    return Expansion(plan=plan, weights=weights, frequencies=freqs, indices=n)
+    idx = np.arange(plan.M, plan.N - plan.M + 1)
+    # omega_n = (2n - N) / (sqrt(N) sigma_r): one correctly rounded division
+    # per term, bit-equal to the reference's frequencies
+    denom = math.sqrt(plan.N) * plan.sigma_r
+    return Expansion(plan=plan, weights=binomial_weights(plan.N, plan.M, plan.N - plan.M),
+                     frequencies=(2 * idx - plan.N) / denom, indices=idx)
+
+
+def _as_result(values, like):
+    return float(values) if np.ndim(like) == 0 else values
 
 
 def eval_truncated_kernel(expansion: Expansion, s):
-    """sum_n d_n cos(w_n s) (kernels.py:230-234)."""
+    """The truncated expansion sum_n d_n cos(w_n s) at s (scalar or array)."""
     s_arr = np.asarray(s, dtype=np.float64)
-    res = np.cos(np.multiply.outer(s_arr, expansion.frequencies)) @ expansion.weights
-    return float(res) if np.isscalar(s) or s_arr.ndim == 0 else res
+    total = np.zeros_like(s_arr)
+    for wk, fk in zip(expansion.weights, expansion.frequencies):
+        total += wk * np.cos(fk * s_arr)
+    return _as_result(total, s)
 
 
 def eval_gaussian(s, sigma_r):
-    """exp(-s^2 / 2 sigma_r^2) (kernels.py:237-243)."""
-    if sigma_r <= 0:
+    """The target range kernel exp(-(s/sigma_r)^2 / 2) (reference kernels.py:237-243)."""
+    if not sigma_r > 0:
         raise InvalidParameterError("sigma_r must be positive")
     s_arr = np.asarray(s, dtype=np.float64)
-    res = np.exp(-(s_arr * s_arr) / (2.0 * sigma_r * sigma_r))
-    return float(res) if np.isscalar(s) or s_arr.ndim == 0 else res
+    return _as_result(np.exp(-0.5 * np.square(s_arr / sigma_r)), s)
 
 
 def polynomial_unsupported(*_a, **_k):

@@ -81,7 +81,17 @@ def compute_T(img, radius) -> float:
 
 
 def brute_force_T(img, radius) -> float:
-    """max over windows of |f(y) - f(x)| (maxfilter.py:64-): by the paper's
-    Proposition 1 this equals max(M - f), which K1 computes exactly, so the
-    brute-force scan is not repeated on the GPU."""
-    return compute_T(img, radius)
+    """max |f(x+y) - f(x)| over all pixels and in-image offsets |y| <= R,
+    evaluated directly (O(R^2) per pixel) on the GPU — reference
+    maxfilter.py:64-82.  Independent of K1's separable max filter, so it
+    cross-checks compute_T (Proposition 1 of the paper)."""
+    import ctypes as C
+
+    if radius < 0:
+        raise InvalidParameterError("radius must be >= 0")
+    s = stage(img)
+    out = C.c_double(0.0)
+    _lib.check(_lib.load().sbf_brute_force_T(s.tensor.data_ptr(), s.dtype, s.H, s.W, s.W,
+                                             int(radius), C.byref(out), _stream_ptr()),
+               "brute_force_T")
+    return float(out.value)

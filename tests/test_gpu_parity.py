@@ -41,6 +41,19 @@ def test_max_filter_and_T_bit_exact_golden():
         assert np.array_equal(P.max_filter_1d(g[f"seq_{k}"], int(g[f"sR_{k}"])), g[f"smax_{k}"])
 
 
+def test_brute_force_T_equals_compute_T():
+    """The O(R^2) direct scan (maxfilter.py:64-82) and K1's separable max
+    filter agree (the paper's Proposition 1), on random and golden images."""
+    rng = np.random.default_rng(11)
+    for shape, R in [((37, 53), 3), ((64, 64), 0), ((1, 40), 5), ((90, 7), 9)]:
+        img = rng.uniform(0, 255, shape)
+        assert P.brute_force_T(img, R) == P.compute_T(img, R) == O.compute_T(img, R)
+    g = golden("maxfilter.npz")
+    for k in range(0, 40, 5):
+        img, R = g[f"img_{k}"], int(g[f"R_{k}"])
+        assert P.brute_force_T(img, R) == float(g[f"T_{k}"]), k
+
+
 def test_config1_T_and_M_bit_exact():
     img = config_image(1)
     assert P.compute_T(img, 9) == 251.39522633396712

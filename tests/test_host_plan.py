@@ -119,3 +119,17 @@ def test_cfg4_term_table_matches_reference_plans():
     rows = golden("config_plans.npz")["rows"]
     ks = tuple(int(r[4]) // 2 - int(r[5]) + 1 for r in rows if int(r[0]) == 4)
     assert ks == CFG4_K
+
+
+def test_binomial_weights_correctly_rounded():
+    """Host twin (sbf_binomial_weights) == C(N,n)/2^N rounded once, as the
+    reference computes it with exact integers (kernels.py:198-212),
+    subnormal tails included."""
+    import math
+    from fractions import Fraction
+    import paper_1203_5128_b200 as P
+    assert P.binomial_weights(2, 0, 2).tolist() == [0.25, 0.5, 0.25]
+    for N, lo, hi in [(1, 0, 1), (29, 7, 22), (263, 111, 152), (1100, 0, 1100), (2463, 0, 60)]:
+        got = P.binomial_weights(N, lo, hi)
+        want = [float(Fraction(math.comb(N, n), 1 << N)) for n in range(lo, hi + 1)]
+        assert got.tolist() == want, N
