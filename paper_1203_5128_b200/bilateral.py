@@ -253,7 +253,7 @@ def _filter_on_device(s, params: FilterParams, out_f64: bool, to_host: bool = Fa
     return out, _plan_from_struct(plan_c), fallbacks
 
 
-def shiftable_bf_batch(imgs, params: FilterParams, lanes: int = 3, out=None):
+def shiftable_bf_batch(imgs, params: FilterParams, lanes: int = 3, out=None, stage: str = "ce"):
     """`[shiftable_bf(img, params) for img in imgs]`, pipelined on the GPU.
 
     A batch of independent images (the config-4 workload) is the same call
@@ -268,7 +268,11 @@ def shiftable_bf_batch(imgs, params: FilterParams, lanes: int = 3, out=None):
     `imgs`: torch tensors — page-locked host tensors (float32/float64) or
     CUDA tensors; other inputs go through `shiftable_bf` one by one.
     `out`: optional list of result tensors (same shape, float dtype of the
-    input, same side) to write into.
+    input, same side) to write into.  `stage`: how host images reach the
+    device — "ce" (copy engine, cudaMemcpyAsync: overlaps the other lanes'
+    kernels without taking SMs) or "sm" (the SMs read page-locked memory,
+    sbf_stage_h2d).  Host results come back by the copy engine from a lane
+    buffer, so both PCIe directions overlap the kernels.
     """
     import torch
 
@@ -304,7 +308,7 @@ def shiftable_bf_batch(imgs, params: FilterParams, lanes: int = 3, out=None):
         for _ in range(lanes):
             s = torch.cuda.Stream(device=dev)
             s.wait_event(start)
-            lane.append({"stream": s, "ws": None, "inp": None})
+            lane.append({"stream": s, "ws": None, "inp": None, "res": None})
         for i, (t, o) in enumerate(zip(imgs, outs)):
             ln = lane[i % lanes]
             H, W = int(t.shape[0]), int(t.shape[1])
@@ -321,17 +325,33 @@ def shiftable_bf_batch(imgs, params: FilterParams, lanes: int = 3, out=None):
                     b = ln["inp"]
                     if b is None or b.shape != t.shape or b.dtype != t.dtype:
                         b = ln["inp"] = torch.empty(t.shape, dtype=t.dtype, device=dev)
-                    b.copy_(t, non_blocking=True)
+                    if stage == "sm":
+                        _lib.check(lib.sbf_stage_h2d(t.data_ptr(),
+                                                     _lib.STAGE_F64 if dt == _lib.SBF_F64 else _lib.STAGE_F32,
+                                                     t.numel(), b.data_ptr(), ln["stream"].cuda_stream),
+                                   "stage_h2d")
+                    else:
+                        b.copy_(t, non_blocking=True)
                     src = b
                 m = metas[i]
+                dst = o
+                if not o.is_cuda:
+                    # the result lands in a lane buffer and goes back by the
+                    # copy engine, overlapping the other lanes' kernels
+                    r = ln["res"]
+                    if r is None or r.shape != o.shape or r.dtype != o.dtype:
+                        r = ln["res"] = torch.empty(o.shape, dtype=o.dtype, device=dev)
+                    dst = r
                 _lib.check(lib.sbf_shiftable_bf(
                     src.data_ptr(), dt, H, W, sp, radius,
                     float(params.fixed_T) if use_fixed else -1.0, float(params.sigma_r),
-                    float(params.epsilon), rule, l2e, prec, o.data_ptr(),
+                    float(params.epsilon), rule, l2e, prec, dst.data_ptr(),
                     _lib.SBF_F64 if o.dtype == torch.float64 else _lib.SBF_F32,
                     m.data_ptr() + _META_PLAN, m.data_ptr() + _META_STATS,
                     m.data_ptr() + _META_FB, TERMS_CAP, ln["ws"].data_ptr(), total,
                     ln["stream"].cuda_stream), "shiftable_bf")
+                if dst is not o:
+                    o.copy_(dst, non_blocking=True)
                 metas_h[i].copy_(m, non_blocking=True)
         for ln in lane:
             main.wait_stream(ln["stream"])
