@@ -91,11 +91,13 @@ class StripFilter:
     `bufs` are CUDA tensors (rows x W, float32/float64) holding image rows
     [strip.buf_lo, strip.buf_hi) of channels of height `img_H`.  `run()`
     performs K1 per channel, ONE max-allreduce of all channel T values,
-    then K2/K3/K4 per channel; it never synchronises the host.
+    then the plan and the filter per channel, stream-ordered; `check()`
+    reads plans, statistics and fallback counts back once (non-finite input,
+    HDR re-run, ambiguous order) — the shiftable_bf semantics.
     """
 
     def __init__(self, bufs, strip: Strip, img_H: int, params: FilterParams,
-                 reduce_max: Optional[Callable] = None, precision: str = "fp32",
+                 reduce_max: Optional[Callable] = None, precision: Optional[str] = None,
                  overlap: bool = False):
         import torch
         self.lib = _lib.load()
@@ -107,7 +109,11 @@ class StripFilter:
         self.dev = self.bufs[0].device
         self.sp = to_c_spatial(params.resolved_spatial())
         self.R = params.resolved_radius()
-        self.prec = _lib.PREC_HDR if precision == "hdr" else _lib.PREC_FP32
+        # the filter's precision mode: params.precision unless overridden;
+        # "auto" runs the fp32 kernels with the device-side range guard
+        # (check() re-runs a flagged channel on the fp64 path)
+        mode = precision if precision is not None else params.precision
+        self.prec = {"fp32": _lib.PREC_FP32, "hdr": _lib.PREC_HDR}.get(mode, _lib.PREC_AUTO)
         self.dt = [_lib.SBF_F64 if b.dtype == torch.float64 else _lib.SBF_F32 for b in self.bufs]
         C = len(self.bufs)
         H, W = self.bufs[0].shape
@@ -181,17 +187,60 @@ class StripFilter:
                 float(p.fixed_T) if use_fixed else 0.0, float(p.sigma_r), float(p.epsilon),
                 _lib.RULES[p.truncation], log_2_over_eps(p.epsilon), self.plans[c].data_ptr(),
                 self.terms[c].data_ptr(), TERMS_CAP, cst), "plan")
-            _lib.check(lib.sbf_filter(
-                b.data_ptr(), self.dt[c], self.H, self.W, self.W, s.buf_lo, self.img_H, lo, hi,
-                self.sp, self.plans[c].data_ptr(), self.terms[c].data_ptr(),
-                self.stats[c].data_ptr(), self.prec, self.out[c].data_ptr(), self.dt[c],
-                self.fb[c:c + 1].data_ptr(), ws.data_ptr(), ws.numel(), cst), "filter")
+            self._filter_channel(c, cst, ws, self.prec)
         if self.overlap:
             for c in range(len(self.bufs)):
                 e = torch.cuda.Event()
                 e.record(self.side[c])
                 main.wait_event(e)
         return self.out
+
+    def check(self, stream_ptr=None):
+        """Host-side validation after run()/finish() (one read-back of the
+        plans, statistics and fallback counts; synchronises the stream):
+        raises InvalidParameterError on non-finite input or a failed plan,
+        re-runs a channel the device flagged (HDR range guard, or an order
+        whose ceil(0.405 q^2) is ambiguous at 2 ulp — re-planned with the host
+        twin), and returns [(KernelPlan, fallback_pixels)] per channel, with a
+        RuntimeWarning for fallbacks, like shiftable_bf."""
+        import warnings
+
+        import torch
+
+        from .kernels import select_plan
+
+        st = self._stream(stream_ptr)
+        torch.cuda.ExternalStream(st, device=self.dev).synchronize()
+        out = []
+        stats = self.stats.cpu().numpy()
+        for c in range(len(self.bufs)):
+            if int(stats[c, 7:8].view(np.uint64)[0]) != 0:
+                raise InvalidParameterError(f"channel {c} contains non-finite samples")
+            pl = _lib.SbfPlan.from_buffer_copy(self.plans[c].cpu().numpy().tobytes())
+            _lib.check(pl.status, "plan")
+            p = self.params
+            if pl.flags & (_lib.PLAN_NEEDS_HDR | _lib.PLAN_N_AMBIGUOUS):
+                prec = _lib.PREC_HDR if pl.flags & _lib.PLAN_NEEDS_HDR else self.prec
+                if pl.flags & _lib.PLAN_N_AMBIGUOUS:
+                    ph = select_plan(pl.T, p.sigma_r, p.epsilon, truncation=p.truncation)
+                    use_fixed = p.fixed_T is not None
+                    _lib.check(self.lib.sbf_plan_device_forced(
+                        self.T[c:c + 1].data_ptr(), 1 if use_fixed else 0,
+                        float(p.fixed_T) if use_fixed else 0.0, float(p.sigma_r),
+                        float(p.epsilon), _lib.RULES[p.truncation], log_2_over_eps(p.epsilon),
+                        ph.N, ph.M, self.plans[c].data_ptr(), self.terms[c].data_ptr(),
+                        TERMS_CAP, st), "plan")
+                self.fb[c:c + 1].zero_()
+                torch.cuda.current_stream(self.dev).synchronize()
+                self._filter_channel(c, st, self.ws, prec)
+                torch.cuda.ExternalStream(st, device=self.dev).synchronize()
+                pl = _lib.SbfPlan.from_buffer_copy(self.plans[c].cpu().numpy().tobytes())
+            fb = int(self.fb[c].item())
+            if fb:
+                warnings.warn(f"channel {c}: {fb} pixel(s) had a non-positive normalizer; "
+                              "input values kept", RuntimeWarning, stacklevel=2)
+            out.append((_plan_from_struct(pl), fb))
+        return out
 
     def launches_per_run(self):
         """Kernels one run() launches: per channel K1 (row + column pass), the
@@ -202,6 +251,15 @@ class StripFilter:
             K = pl.N // 2 - pl.M + 1
             n += 3 + (2 * K + 1 if self.sp.r >= 9 else 2)
         return n
+
+    def _filter_channel(self, c, st, ws, prec):
+        s = self.strip
+        lo, hi = s.out_lo - s.buf_lo, s.out_hi - s.buf_lo
+        _lib.check(self.lib.sbf_filter(
+            self.bufs[c].data_ptr(), self.dt[c], self.H, self.W, self.W, s.buf_lo, self.img_H, lo,
+            hi, self.sp, self.plans[c].data_ptr(), self.terms[c].data_ptr(),
+            self.stats[c].data_ptr(), prec, self.out[c].data_ptr(), self.dt[c],
+            self.fb[c:c + 1].data_ptr(), ws.data_ptr(), ws.numel(), st), "filter")
 
     def plans_host(self):
         return [_plan_from_struct(_lib.SbfPlan.from_buffer_copy(self.plans[c].cpu().numpy().tobytes()))
