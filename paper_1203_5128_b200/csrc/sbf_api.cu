@@ -217,18 +217,22 @@ static size_t sweep_ws(const SweepEntry& w, int64_t H, int64_t W, int64_t rows_o
   return sweep_zero_bytes(w, W, rows_out) + align_up((size_t)(H * ldp) * 4);
 }
 
+static size_t split_ws_core(int64_t H, int64_t W, int64_t rows_out, int dtype) {
+  size_t bytes = align_up((size_t)(rows_out * W) * 8) + align_up((size_t)(rows_out * W) * 16);
+  if (dtype == SBF_F64) bytes += align_up((size_t)(H * W) * 4);
+  return bytes;
+}
+
 // partial accumulators (+ an fp32 centred copy of float64 inputs for K3)
 size_t filter_ws(int64_t H, int64_t W, int64_t rows_out, int dtype, const sbf_spatial* sp,
                  int precision) {
   if (precision == SBF_PREC_AUTO)  // either path may run
     return smax(filter_ws(H, W, rows_out, dtype, sp, SBF_PREC_FP32),
                 filter_ws(H, W, rows_out, dtype, sp, SBF_PREC_HDR));
-  if (find_split(*sp, precision)) {
-    // split sweep: accumulator + column-smoothed images of one term
-    size_t bytes = align_up((size_t)(rows_out * W) * 8) + align_up((size_t)(rows_out * W) * 16);
-    if (dtype == SBF_F64) bytes += align_up((size_t)(H * W) * 4);
-    return bytes;
-  }
+  if (find_split(*sp, precision))
+    // split sweep: accumulator, column-smoothed images of one term, the
+    // fp32 view of float64 inputs, the work queue (<= rows_out / 32 bands)
+    return split_ws_core(H, W, rows_out, dtype) + align_up((size_t)(64 + 2 * (rows_out / 32 + 2)) * 4);
   if (const SweepEntry* w = find_sweep(*sp, precision)) return sweep_ws(*w, H, W, rows_out);
   const TermsEntry* e = find_entry(*sp, precision);
   if (!e) return align_up((size_t)(rows_out * W) * 16);  // generic: one fp64 accumulator
@@ -517,17 +521,26 @@ static int launch_split_path(const FilterLaunch& a, const SplitEntry& se, int r,
   const int64_t want = 4 * 148;
   const int64_t nb = smax<int64_t>(1, (want + cgroups - 1) / cgroups);
   p.band = (int)smin<int64_t>(smax<int64_t>(8 * halo, (rows_out + nb - 1) / nb), 1024);
+  p.band = (p.band + 31) / 32 * 32;  // whole SH row groups per band
   const int64_t rgroups = (rows_out + 31) / 32;
   const int64_t ns = smax<int64_t>(1, (want + rgroups - 1) / rgroups);
   p.seg = (int)smax<int64_t>(16 * halo, (a.W + ns - 1) / ns);
-  sbf_plan plan;
-  SBF_CHECK_CUDA(cudaMemcpyAsync(&plan, a.plan, sizeof(plan), cudaMemcpyDeviceToHost, a.stream));
-  SBF_CHECK_CUDA(cudaStreamSynchronize(a.stream));
-  const int K = plan.status == SBF_OK ? plan.K_eval : 0;
+  p.svx = (int)cgroups;
+  p.svy = (int)((rows_out + p.band - 1) / p.band);
+  p.shx = (int)rgroups;
+  p.shy = (int)((a.W + p.seg - 1) / p.seg);
+  p.hdr_guard = g_hdr_guard;
+  // the work queue and its per-band counters follow the f32 view
+  int* q = reinterpret_cast<int*>(ws + split_ws_core(a.H, a.W, rows_out, a.dtype));
+  p.head = q;
+  p.sv_done = q + 64;
+  p.sh_done = q + 64 + p.svy;
   if (g_stage_mask & 1) {
-    if (K == 0) SBF_CHECK_CUDA(cudaMemsetAsync(p.nd, 0, nd_bytes, a.stream));
-    int rc = se.launch(p, K, a.stream);
+    SBF_CHECK_CUDA(cudaMemsetAsync(q, 0, (size_t)(64 + 2 * p.svy) * sizeof(int), a.stream));
+    if (g_k3_ev[0]) SBF_CHECK_CUDA(cudaEventRecord(g_k3_ev[0], a.stream));
+    int rc = se.launch(p, a.stream);  // every term, count read on the device
     if (rc != SBF_OK) return rc;
+    if (g_k3_ev[1]) SBF_CHECK_CUDA(cudaEventRecord(g_k3_ev[1], a.stream));
   }
   if (!(g_stage_mask & 2)) return SBF_OK;
   return launch_epilogue<float>(a, reinterpret_cast<const float*>(p.nd), 1, rows_out * a.W);
@@ -675,7 +688,7 @@ int launch_filter(const FilterLaunch& a) {
     FilterLaunch b = a;
     b.precision = SBF_PREC_FP32;
     const TermsEntry* e3 = find_entry(b.sp, SBF_PREC_FP32);
-    if ((!e3 && !find_sweep(b.sp, SBF_PREC_FP32)) || find_split(b.sp, SBF_PREC_FP32)) {
+    if (!e3 && !find_sweep(b.sp, SBF_PREC_FP32) && !find_split(b.sp, SBF_PREC_FP32)) {
       double st[8];
       SBF_CHECK_CUDA(cudaMemcpyAsync(st, a.stats, sizeof(st), cudaMemcpyDeviceToHost, a.stream));
       SBF_CHECK_CUDA(cudaStreamSynchronize(a.stream));

@@ -33,8 +33,14 @@ struct SplitParams {
   float2* nd;  // [rows_out][W] (num, den)
   int term;
   int first;
-  int band;  // SV output rows per CTA
+  int band;  // SV output rows per CTA (a multiple of SH_ROWS)
   int seg;   // SH output columns per CTA
+  int hdr_guard;  // SBF_PREC_AUTO: flag the plan and do nothing on wide ranges
+  // device work queue of the persistent sweep (zeroed before the launch)
+  int* head;
+  int* sv_done;  // per band: SV tiles finished, all terms so far
+  int* sh_done;  // per band: SH tiles finished, all terms so far
+  int svx, svy, shx, shy;
 };
 
 template <int R, int PASSES>
@@ -64,8 +70,7 @@ struct SplitCfg {
 #endif
 
 template <int R, int PASSES>
-__global__ void __launch_bounds__(SplitCfg<R, PASSES>::SV_THREADS, SBF_SV_MINB)
-    sv_kernel(const SplitParams p) {
+__device__ __forceinline__ void sv_tile(const SplitParams& p, const int bx, const int by) {
   using C = SplitCfg<R, PASSES>;
   constexpr int D = C::D, L = C::L, HALO = C::HALO, IMGS = C::IMGS, GOFF = C::GOFF;
   constexpr int THREADS = C::SV_THREADS, TPC = 4 / IMGS;
@@ -74,14 +79,12 @@ __global__ void __launch_bounds__(SplitCfg<R, PASSES>::SV_THREADS, SBF_SV_MINB)
   const int gv_len = p.band + 2 * HALO + GOFF;
   float* FR = gv + gv_len + 4;
 
-  const sbf_plan* plan = p.plan;
-  if (plan->status != SBF_OK || p.term >= plan->K_eval) return;
   const int tid = threadIdx.x;
   const float centerf = p.centred ? 0.f : (float)p.stats[3];
   const float a = p.a, b = p.b;
   const float nu = (float)p.terms[p.term].turns;
 
-  const int y0 = p.out_lo + blockIdx.y * p.band;
+  const int y0 = p.out_lo + by * p.band;
   const int y1 = min(p.out_hi, y0 + p.band);
   const int Bn = y1 - y0;
   const int T_total = Bn + 2 * HALO;
@@ -95,7 +98,7 @@ __global__ void __launch_bounds__(SplitCfg<R, PASSES>::SV_THREADS, SBF_SV_MINB)
   __syncthreads();
 
   const int q = tid / TPC, pair = tid % TPC;
-  const int col = blockIdx.x * C::SV_COLS + q;
+  const int col = bx * C::SV_COLS + q;
   const bool colok = col < p.W;
   const int colc = colok ? col : p.W - 1;
   const float* fcol = p.f + (int64_t)(y0 - HALO) * p.ld + colc;
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(SplitCfg<R, PASSES>::SV_THREADS, SBF_SV_MINB)
 // positions mod RINGC relative to the segment start; an output replaces its
 // own input (position s - HALO) in place.
 template <int R, int PASSES>
-__global__ void __launch_bounds__(128) sh_kernel(const SplitParams p) {
+__device__ __forceinline__ void sh_tile(const SplitParams& p, const int bx, const int by) {
   using C = SplitCfg<R, PASSES>;
   constexpr int D = C::D, L = C::L, HALO = C::HALO, IMGS = C::IMGS, GOFF = C::GOFF;
   constexpr int TILE = C::TILE, NTILE = C::NTILE, RINGC = C::RINGC, RP = C::RPITCH;
@@ -201,11 +204,9 @@ __global__ void __launch_bounds__(128) sh_kernel(const SplitParams p) {
   float* gL = ring + ROWS * RP;                     // factors at stream positions [s0 - GOFF, s0 + GE)
   float* gR = gL + GE + GOFF;                       // factors at [sR0 - GOFF, sR0 + GE + GOFF)
 
-  const sbf_plan* plan = p.plan;
-  if (plan->status != SBF_OK || p.term >= plan->K_eval) return;
   const int tid = threadIdx.x;
   const int W = p.W;
-  const int c0 = blockIdx.y * p.seg;
+  const int c0 = by * p.seg;
   const int s0 = c0;
   const int s1 = min(c0 + p.seg + 2 * HALO, W + 2 * HALO);
   const int sR0 = max(s0, s1 - GE);
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(128) sh_kernel(const SplitParams p) {
   const float scale = (float)term.scale;
   const float nu = (float)term.turns;
   const float centerf = p.centred ? 0.f : (float)p.stats[3];
-  const int r0 = p.out_lo + blockIdx.x * ROWS;  // first buffer row of this CTA
+  const int r0 = p.out_lo + bx * ROWS;  // first buffer row of this CTA
   const int nrows = min(ROWS, p.out_hi - r0);
   const float* Ub = p.U + (int64_t)(r0 - p.out_lo) * W * 4;
 
@@ -300,7 +301,8 @@ __global__ void __launch_bounds__(128) sh_kernel(const SplitParams p) {
         const int c = s_lo + cc - 2 * HALO;
         const int64_t row = r0 + rr;
         fpx[i] = __ldg(p.f + row * p.ld + c);
-        if (!p.first) acc_old[i] = p.nd[(row - p.out_lo) * W + c];
+        // (num, den) of the previous term, written by another CTA: from L2
+        if (!p.first) acc_old[i] = __ldcg(p.nd + (row - p.out_lo) * W + c);
       }
     }
     if (j + 1 < ntiles)
@@ -366,32 +368,105 @@ size_t sh_smem_bytes() {
   return (size_t)C::SH_ROWS * C::RPITCH * 4 + (size_t)2 * (C::GEDGE + C::GOFF) * 4 + 16;
 }
 
-// all terms: SV then SH per term; nd is fully (re)written by the first term
+__device__ __forceinline__ void split_wait(const int* ctr, int target) {
+  if (threadIdx.x == 0) {
+    int v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if (v >= target) break;
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+// Every term in one persistent launch with a device work queue: items are
+// taken in order [SV tiles of term 0 | SH tiles of term 0 | SV tiles of term
+// 1 | ...], the term count is read from the device plan (no host round
+// trip; graph-capturable).  Dependencies are per row band and only ever on
+// items taken earlier, so the queue cannot deadlock:
+//  * SH(k) tiles of band b wait for all SV(k) tiles of band b (U is complete)
+//    and for all SH(k-1) tiles of band b ((num, den) updated in term order:
+//    one owner per pixel and term, a fixed sum order);
+//  * SV(k) tiles of band b wait for all SH(k-1) tiles of band b (U, written
+//    once per term, has been consumed).
 template <int R, int PASSES>
-int launch_split(const SplitParams& base_p, int K_eval, cudaStream_t st) {
+__global__ void __launch_bounds__(128) split_queue_kernel(SplitParams p) {
   using C = SplitCfg<R, PASSES>;
-  const size_t svs = sv_smem_bytes<R, PASSES>(base_p.band), shs = sh_smem_bytes<R, PASSES>();
-  SBF_CHECK_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(sv_kernel<R, PASSES>), svs));
-  SBF_CHECK_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(sh_kernel<R, PASSES>), shs));
-  const int rows_out = base_p.out_hi - base_p.out_lo;
-  const dim3 svg((unsigned)((base_p.W + C::SV_COLS - 1) / C::SV_COLS),
-                 (unsigned)((rows_out + base_p.band - 1) / base_p.band));
-  const dim3 shg((unsigned)((rows_out + C::SH_ROWS - 1) / C::SH_ROWS),
-                 (unsigned)((base_p.W + base_p.seg - 1) / base_p.seg));
-  for (int k = 0; k < K_eval; ++k) {
-    SplitParams p = base_p;
+  static_assert(C::SV_THREADS == 128, "SV and SH tiles share the CTA shape");
+  __shared__ int s_item;
+  pdl_wait();
+  const sbf_plan* plan = p.plan;
+  if (plan->status != SBF_OK) return;
+  if (p.hdr_guard && needs_hdr(p.stats)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(const_cast<int*>(&plan->flags), SBF_PLAN_NEEDS_HDR);
+    return;
+  }
+  const int K = plan->K_eval;
+  const int rows_out = p.out_hi - p.out_lo;
+  if (K == 0) {  // no retained term: (num, den) = 0, every pixel falls back
+    const int64_t n = (int64_t)rows_out * p.W;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+      p.nd[i] = make_float2(0.f, 0.f);
+    return;
+  }
+  const int n_sv = p.svx * p.svy, n_sh = p.shx * p.shy;
+  const int per = n_sv + n_sh;
+  const long long total = (long long)K * per;
+  const int gpb = p.band / C::SH_ROWS;  // SH row groups per band
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(p.head, 1);
+    __syncthreads();
+    const long long item = s_item;
+    __syncthreads();  // s_item is rewritten by the next pull
+    if (item >= total) break;
+    const int k = (int)(item / per), j = (int)(item - (long long)k * per);
     p.term = k;
     p.first = k == 0;
-    sv_kernel<R, PASSES><<<svg, C::SV_THREADS, svs, st>>>(p);
-    sh_kernel<R, PASSES><<<shg, 128, shs, st>>>(p);
+    if (j < n_sv) {
+      const int bx = j % p.svx, band = j / p.svx;
+      const int rows_b = min(p.band, rows_out - band * p.band);
+      const int nsh_b = ((rows_b + C::SH_ROWS - 1) / C::SH_ROWS) * p.shy;
+      if (k > 0) split_wait(p.sh_done + band, k * nsh_b);
+      sv_tile<R, PASSES>(p, bx, band);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) atomicAdd(p.sv_done + band, 1);
+    } else {
+      const int jj = j - n_sv;
+      const int rx = jj / p.shy, sy = jj - rx * p.shy;
+      const int band = rx / gpb;
+      const int rows_b = min(p.band, rows_out - band * p.band);
+      const int nsh_b = ((rows_b + C::SH_ROWS - 1) / C::SH_ROWS) * p.shy;
+      split_wait(p.sv_done + band, (k + 1) * p.svx);
+      if (k > 0) split_wait(p.sh_done + band, k * nsh_b);
+      sh_tile<R, PASSES>(p, rx, sy);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) atomicAdd(p.sh_done + band, 1);
+    }
   }
+}
+
+template <int R, int PASSES>
+int launch_split(const SplitParams& p, cudaStream_t st) {
+  const size_t smem = smax(sv_smem_bytes<R, PASSES>(p.band), sh_smem_bytes<R, PASSES>());
+  SBF_CHECK_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(split_queue_kernel<R, PASSES>), smem));
+  int per_sm = 0;
+  SBF_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, split_queue_kernel<R, PASSES>,
+                                                               128, smem));
+  SBF_REQUIRE(per_sm > 0, SBF_ERR_CUDA, "split sweep: no CTA fits on an SM");
+  // an ordinary launch: the queue counters are cleared by a memset just
+  // before, which a programmatic (early) launch would not wait for
+  split_queue_kernel<R, PASSES><<<dim3((unsigned)(per_sm * device_sm_count())), 128, smem, st>>>(p);
   SBF_CHECK_LAUNCH();
   return SBF_OK;
 }
 
 struct SplitEntry {
   int r, passes;
-  int (*launch)(const SplitParams&, int, cudaStream_t);
+  int (*launch)(const SplitParams&, cudaStream_t);
 };
 
 #define SBF_SPLIT_ENTRY(R, P) \

@@ -140,7 +140,15 @@ class StripFilter:
 
     def _stream(self, stream_ptr):
         import torch
-        return stream_ptr if stream_ptr is not None else torch.cuda.current_stream().cuda_stream
+        return stream_ptr if stream_ptr is not None else torch.cuda.current_stream(self.dev).cuda_stream
+
+    def _stream_obj(self, stream_ptr):
+        """The torch stream object of `stream_ptr` (the current stream when
+        None: wrapping its raw handle would not order the null stream)."""
+        import torch
+        if stream_ptr is None:
+            return torch.cuda.current_stream(self.dev)
+        return torch.cuda.ExternalStream(stream_ptr, device=self.dev)
 
     def local_T(self, stream_ptr=None):
         """K1 on every channel; returns the device tensor of strip-local T values."""
@@ -174,7 +182,7 @@ class StripFilter:
         self.fb.zero_()
         if self.overlap:
             import torch
-            main = torch.cuda.ExternalStream(st, device=self.dev)
+            main = self._stream_obj(stream_ptr)
             ev = torch.cuda.Event()
             ev.record(main)
         for c, b in enumerate(self.bufs):
@@ -210,7 +218,7 @@ class StripFilter:
         from .kernels import select_plan
 
         st = self._stream(stream_ptr)
-        torch.cuda.ExternalStream(st, device=self.dev).synchronize()
+        self._stream_obj(stream_ptr).synchronize()
         out = []
         stats = self.stats.cpu().numpy()
         for c in range(len(self.bufs)):
@@ -233,7 +241,7 @@ class StripFilter:
                 self.fb[c:c + 1].zero_()
                 torch.cuda.current_stream(self.dev).synchronize()
                 self._filter_channel(c, st, self.ws, prec)
-                torch.cuda.ExternalStream(st, device=self.dev).synchronize()
+                self._stream_obj(stream_ptr).synchronize()
                 pl = _lib.SbfPlan.from_buffer_copy(self.plans[c].cpu().numpy().tobytes())
             fb = int(self.fb[c].item())
             if fb:
