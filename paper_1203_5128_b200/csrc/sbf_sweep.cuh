@@ -613,34 +613,47 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
     if (ndone > 0) {
       const int xlim = min(WC, p.W - strip * WC);
       unsigned long long bad = 0;
-      for (int d = 0; d < ndone; ++d) {
-        const int r0 = s_done[d] * SEGR, r1 = min(rows_all, r0 + SEGR);
-        for (int i = tid; i < (r1 - r0) * xlim; i += THREADS) {
-          const int rr = r0 + i / xlim, col = strip * WC + i % xlim;
-          const int64_t ai = (int64_t)rr * p.W + col;
-          const long long sum = (long long)__ldcg(p.acc + ai);
-          const int lo = (int)(unsigned)(sum & 0xffffffffll);
-          const long long hi = (sum - (long long)lo) >> 32;
-          const double num = (double)hi * inv_nscale, den = (double)lo * inv_dscale;
-          const bool is_bad = !(den > 0.0);  // bilateral.py:244 (NaN counts as bad)
-          bad += is_bad ? 1 : 0;
-          const int64_t fi = (int64_t)(p.out_lo + rr) * p.fo_ld + col;
-          if (p.out_dtype == SBF_F32) {
-            float o;
-            if (is_bad)
-              o = p.fo_dtype == SBF_F32 ? static_cast<const float*>(p.fo)[fi]
-                                        : (float)static_cast<const double*>(p.fo)[fi];
-            else
-              o = (float)(num / den) + centerf;
-            static_cast<float*>(p.out)[ai] = o;
-          } else {
-            double o;
-            if (is_bad)
-              o = p.fo_dtype == SBF_F32 ? (double)static_cast<const float*>(p.fo)[fi]
-                                        : static_cast<const double*>(p.fo)[fi];
-            else
-              o = num / den + centerd;
-            static_cast<double*>(p.out)[ai] = o;
+      // thread per output column; each thread issues EPI_U accumulator loads
+      // (L2) before it consumes any, so the segment's loads overlap
+      constexpr int EPI_U = 8;
+      if (tid < xlim) {
+        const int col = strip * WC + tid;
+        for (int d = 0; d < ndone; ++d) {
+          const int r0 = s_done[d] * SEGR, nr = min(rows_all, r0 + SEGR) - r0;
+          for (int v0 = 0; v0 < nr; v0 += EPI_U) {
+            long long sum[EPI_U];
+#pragma unroll
+            for (int u = 0; u < EPI_U; ++u)
+              sum[u] = v0 + u < nr ? (long long)__ldcg(p.acc + (int64_t)(r0 + v0 + u) * p.W + col) : 0;
+#pragma unroll
+            for (int u = 0; u < EPI_U; ++u) {
+              if (v0 + u >= nr) break;
+              const int rr = r0 + v0 + u;
+              const int64_t ai = (int64_t)rr * p.W + col;
+              const int lo = (int)(unsigned)(sum[u] & 0xffffffffll);
+              const long long hi = (sum[u] - (long long)lo) >> 32;
+              const double num = (double)hi * inv_nscale, den = (double)lo * inv_dscale;
+              const bool is_bad = !(den > 0.0);  // bilateral.py:244 (NaN counts as bad)
+              bad += is_bad ? 1 : 0;
+              const int64_t fi = (int64_t)(p.out_lo + rr) * p.fo_ld + col;
+              if (p.out_dtype == SBF_F32) {
+                float o;
+                if (is_bad)
+                  o = p.fo_dtype == SBF_F32 ? static_cast<const float*>(p.fo)[fi]
+                                            : (float)static_cast<const double*>(p.fo)[fi];
+                else
+                  o = (float)(num / den) + centerf;
+                static_cast<float*>(p.out)[ai] = o;
+              } else {
+                double o;
+                if (is_bad)
+                  o = p.fo_dtype == SBF_F32 ? (double)static_cast<const float*>(p.fo)[fi]
+                                            : static_cast<const double*>(p.fo)[fi];
+                else
+                  o = num / den + centerd;
+                static_cast<double*>(p.out)[ai] = o;
+              }
+            }
           }
         }
       }

@@ -284,6 +284,27 @@ def test_direct_bf_full_size_vs_shiftable():
     assert m.mse < 10.0
 
 
+def test_acceptance_6_checker_box30_vs_direct_gaussian():
+    """Reference acceptance criterion 6 (pkg/tests/test_acceptance.py:190-203)
+    on the CUDA path: checkerboard(256, 256, 32), Box(30), sigma_r = 10,
+    eps = 0.005 (the generic fp64 term path: no specialised kernel at r = 30)
+    against the brute-force Gaussian BF with the same box; gates
+    max|diff| <= 1e-2 * 255 and MSE <= -20 dB.  The shiftable output is also
+    held to the C oracle at the north-star tolerance."""
+    from oracle import coracle as CO
+    img = P.checkerboard(256, 256, 32)
+    params = P.FilterParams(sigma_s=30, sigma_r=10, epsilon=0.005, spatial=P.Box(30))
+    res = P.shiftable_bf(img, params)
+    ref = P.direct_bf(img, P.Box(30), P.gaussian_range(10.0))
+    m = P.metrics(res.image, ref)
+    print(f"acceptance 6: max|diff|/peak {m.max_abs / 255:.3g} mse_db {m.mse_db:.1f}")
+    assert m.max_abs <= 1e-2 * 255
+    assert m.mse_db <= -20.0
+    ora = CO.shiftable_bf(img, 30.0, 10.0, 0.005, spatial=("box", 30))
+    assert (res.plan.T, res.plan.N, res.plan.M) == (ora["T"], ora["N"], ora["M"])
+    assert_close_image(res.image, ora["image"])
+
+
 def test_direct_bf_rejects_unsupported():
     with pytest.raises(P.InvalidParameterError):
         P.direct_bf(np.zeros((4, 4)), P.IteratedBox(2.0), P.gaussian_range(10.0), radius=3)
