@@ -444,8 +444,15 @@ def run_ours(args, rank, world, dev):
     # written into page-locked host memory, every byte inside the timed region
     pinned_in = [torch.from_numpy(a).pin_memory() for a in host]
     pinned_out = [torch.empty(a.shape, dtype=t.dtype, pin_memory=True) for a, t in zip(host, imgs)]
+    def e2e_call():
+        if cfg == 4:
+            return P.shiftable_bf_batch(pinned_in, params, lanes=E2E_LANES, out=pinned_out)
+        # one image: the single-image call (SM-staged H2D, result streamed
+        # into page-locked memory by the K3 epilogue)
+        return [P.shiftable_bf(pinned_in[0], params)]
+
     for _ in range(max(1, min(args.warmup, 2))):
-        P.shiftable_bf_batch(pinned_in, params, lanes=E2E_LANES, out=pinned_out)
+        e2e_call()
     torch.cuda.synchronize()
     gc.collect()
     gc.disable()  # no collector pauses inside the timed region
@@ -455,7 +462,7 @@ def run_ours(args, rank, world, dev):
     for _ in range(args.steps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
-        res = P.shiftable_bf_batch(pinned_in, params, lanes=E2E_LANES, out=pinned_out)
+        res = e2e_call()
         b.record(st)
         b.synchronize()
         e2e_ms += a.elapsed_time(b)
@@ -479,9 +486,11 @@ def run_ours(args, rank, world, dev):
         launches=KERNELS_PER_IMAGE * len(imgs) * args.steps,
         e2e=dict(value=e2e_value, unit=UNIT, h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h),
                  ms_per_step=e2e_ms / args.steps,
-                 path="shiftable_bf_batch (4 streams): pinned host images -> copy-engine H2D, "
-                      "kernels, copy-engine D2H of each result into pinned host memory; "
-                      "both PCIe directions overlap other images' kernels"),
+                 path=("shiftable_bf_batch (4 streams): pinned host images -> copy-engine H2D, "
+                       "kernels, copy-engine D2H of each result into pinned host memory; "
+                       "both PCIe directions overlap other images' kernels") if cfg == 4 else
+                      ("shiftable_bf on a pinned host tensor: SM-staged H2D, K1..K3, the K3 "
+                       "epilogue writes the result into pinned host memory, one host sync")),
         roofline=dict(
             bound="fp32", achieved=achieved, peak=PEAK_FP32_NOMINAL, unit="TFLOP/s",
             frac=achieved / PEAK_FP32_NOMINAL, traffic=profile_traffic(cfg),

@@ -4,8 +4,12 @@
  * Drop-in boundary for the hot path of the reference package `shiftbf`
  * (arXiv 1203.5128).  Plain pointers and sizes only: no torch types.  All
  * device pointers are caller-owned; the library never frees them.  Every
- * call is stream-ordered and reentrant (no global mutable state besides a
- * thread-local error string).  Status codes mirror the reference CLI exit
+ * call is stream-ordered and reentrant.  Process-wide state: a thread-local
+ * error string, thread-local tuning switches (sbf_set_* below, for
+ * benchmarks; defaults are the measured best), per-device caches (SM count,
+ * the dual form's weight tables of the last geometry) and, on first use of
+ * a device, a raised release threshold of its default stream-ordered memory
+ * pool (scratch blocks are kept across calls).  Status codes mirror the reference CLI exit
  * codes (reference cli.py:309-314) and map onto its exception types
  * (reference errors.py:4-25):
  *
@@ -183,7 +187,12 @@ int sbf_filter(const void* f, int dtype, int64_t H, int64_t W, int64_t ld,
                unsigned long long* fallback_dev, void* ws, size_t ws_bytes,
                void* stream);
 
-/* Whole pipeline (K1 -> K2 -> K3 -> K4) on device buffers; no host sync.
+/* Whole pipeline (K1 -> K2 -> K3 -> K4) on device buffers.  No host sync
+ * and CUDA-graph capturable on the fp32 paths (the K3 sweep, r <= 5, and the
+ * split sweep, r >= 9, with SBF_PREC_FP32 / SBF_PREC_AUTO).  The fp64 paths
+ * (SBF_PREC_HDR, radii without an fp32 kernel) read the plan on the host to
+ * size their term loop / pick the dual form: they synchronise the stream
+ * and return SBF_ERR_UNSUPPORTED under graph capture.
  * fixed_T < 0 means "compute T with window radius R".  *fallback_dev is set
  * to this call's fallback count (reset by the pipeline, not accumulated). */
 size_t sbf_shiftable_bf_workspace(int64_t H, int64_t W, int dtype,

@@ -683,16 +683,13 @@ int launch_filter(const FilterLaunch& a) {
                   a.precision == SBF_PREC_AUTO,
               SBF_ERR_INVALID, "bad precision mode");
   if (a.precision == SBF_PREC_AUTO) {
-    // the K3 path checks the range on the device; every other path reads
-    // the plan on the host anyway, so it resolves the mode there
+    // the fp32 kernels check the range on the device (and flag the plan);
+    // radii without an fp32 kernel run the fp64 path whatever the range
     FilterLaunch b = a;
     b.precision = SBF_PREC_FP32;
     const TermsEntry* e3 = find_entry(b.sp, SBF_PREC_FP32);
     if (!e3 && !find_sweep(b.sp, SBF_PREC_FP32) && !find_split(b.sp, SBF_PREC_FP32)) {
-      double st[8];
-      SBF_CHECK_CUDA(cudaMemcpyAsync(st, a.stats, sizeof(st), cudaMemcpyDeviceToHost, a.stream));
-      SBF_CHECK_CUDA(cudaStreamSynchronize(a.stream));
-      if (fmax(st[2] - st[3], st[3] - st[1]) > 4096.0) b.precision = SBF_PREC_HDR;
+      b.precision = SBF_PREC_HDR;
       return launch_filter(b);
     }
     g_hdr_guard = 1;
@@ -712,6 +709,13 @@ int launch_filter(const FilterLaunch& a) {
   if (const SweepEntry* w = find_sweep(a.sp, a.precision)) return launch_sweep_path(a, *w, r, alpha);
   const TermsEntry* e = find_entry(a.sp, a.precision);
   if (!e) {
+    // the fp64 paths (HDR, radii without an fp32 kernel) size their term
+    // loop and pick the dual form from a host read of the plan: they cannot
+    // be recorded into a CUDA graph
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    SBF_CHECK_CUDA(cudaStreamIsCapturing(a.stream, &cs));
+    SBF_REQUIRE(cs == cudaStreamCaptureStatusNone, SBF_ERR_UNSUPPORTED,
+                "the fp64 filter path reads the plan on the host and cannot be graph-captured");
     const size_t need = align_up((size_t)(rows_out * a.W) * 16);
     SBF_REQUIRE(a.ws && a.ws_bytes >= need, SBF_ERR_WORKSPACE, "filter workspace too small");
     if (g_dual_mode != 0) {

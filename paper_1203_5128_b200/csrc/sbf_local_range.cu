@@ -12,6 +12,7 @@
 // once (written + read); T, min f and max f are reduced on chip and folded
 // into three 64-bit atomics per CTA.
 #include <cstring>
+#include <type_traits>
 
 #include "sbf_common.cuh"
 #include "sbf_plan_warp.cuh"
@@ -28,6 +29,9 @@ constexpr int kRowSeg = 1024;   // outputs per row-pass CTA
 #endif
 #ifndef SBF_K1_VH_COL
 #define SBF_K1_VH_COL 1
+#endif
+#ifndef SBF_K1_STREAM
+#define SBF_K1_STREAM 1  // one-pass K1 (k1_stream_kernel) where the radius allows
 #endif
 constexpr bool g_k1_vh_row = SBF_K1_VH_ROW;  // van Herk blocks (else the doubling ladder)
 constexpr bool g_k1_vh_col = SBF_K1_VH_COL;
@@ -382,6 +386,293 @@ __global__ void __launch_bounds__(kColTile* kColThreadsY) colmax_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// One-pass K1 ("streamed"): f is read from HBM once.
+//
+// A CTA of kStreamThreads threads owns a strip of TC = threads - 2R output
+// columns and a band of output rows.  Thread i streams input column
+// x0 - R + i down the band plus R rows above and below (samples outside the
+// buffer are -inf, which is exactly the clamped window of the reference):
+//  * vertical van Herk / Gil-Werman: the stream is cut into blocks of
+//    w = 2R+1 rows; a running prefix maximum lives in a register, each
+//    completed block is turned into suffix maxima in place in a shared-memory
+//    ring of two blocks per column, and the window of output row j is
+//    max(suffix[j], prefix[j + 2R]) -- 3 comparisons per sample;
+//  * the vertical maxima of G output rows are staged in shared memory
+//    and the same block decomposition runs along the rows (one thread per
+//    (row, block)), giving M for TC columns;
+//  * M - f in fp64 (maxfilter.py:61), min / max / non-finite count of f, and
+//    the optional M image are produced in the same pass.
+// The block reductions fold into the 64-bit order-preserving atomics of the
+// two-pass kernels; the last CTA finalises the statistics and (fused
+// pipeline) builds the plan.
+constexpr int kStreamThreads = 256;
+template <typename T>
+struct StreamG {  // stream steps per group = rows of f in flight per thread = rows per horizontal batch
+  static constexpr int value = sizeof(T) == 4 ? 16 : 8;
+};
+
+// suffix maxima of one column's completed vertical block, in place (stride
+// st); not inlined: it runs once per block, outside the unrolled steps
+template <typename T>
+__device__ __noinline__ void stream_suffix(T* x, int w, int st) {
+  T m = x[(w - 1) * st];
+  for (int k0 = w - 2; k0 >= 0; k0 -= 8) {
+    T s[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (k0 - q >= 0) s[q] = x[(k0 - q) * st];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (k0 - q >= 0) {
+        m = vmax(m, s[q]);
+        x[(k0 - q) * st] = m;
+      }
+  }
+}
+
+// one row block of the horizontal pass: suffix maxima into sr, prefix
+// maxima in place (8 samples read ahead of each chain of comparisons)
+template <typename T>
+__device__ __forceinline__ void stream_scan_row(T* pr, T* sr, int n) {
+  T m = pr[n - 1];
+  sr[n - 1] = m;
+  for (int k0 = n - 2; k0 >= 0; k0 -= 8) {
+    T s[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (k0 - q >= 0) s[q] = pr[k0 - q];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (k0 - q >= 0) {
+        m = vmax(m, s[q]);
+        sr[k0 - q] = m;
+      }
+  }
+  m = pr[0];
+  for (int k0 = 1; k0 < n; k0 += 8) {
+    T s[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (k0 + q < n) s[q] = pr[k0 + q];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (k0 + q < n) {
+        m = vmax(m, s[q]);
+        pr[k0 + q] = m;
+      }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T neg_inf() {
+  return T(-INFINITY);
+}
+
+template <typename T>
+size_t stream_smem_bytes(int R) {
+  const int w = 2 * R + 1;
+  return (size_t)2 * w * kStreamThreads * sizeof(T) +                    // vertical ring
+         (size_t)2 * StreamG<T>::value * (kStreamThreads + 2) * sizeof(T) +  // prefix / suffix rows
+         64 * sizeof(double);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kStreamThreads, 2) k1_stream_kernel(
+    const T* __restrict__ f, int64_t H, int64_t W, int64_t ld, int R, int band, int64_t t_lo,
+    int64_t t_hi, T* __restrict__ M_out, unsigned long long* __restrict__ red,
+    unsigned* __restrict__ done, const PlanArgs pa) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int NT = kStreamThreads, G = StreamG<T>::value, RB = G, HP = NT + 2;
+  pdl_wait();     // the statistics reset (and f, if a kernel produced it)
+  pdl_trigger();  // K3 may be scheduled; it waits for this grid itself
+  const int w = 2 * R + 1;
+  const int TC = NT - 2 * R;
+  T* ring = reinterpret_cast<T*>(smem_raw);       // [2w][NT]
+  T* hp = ring + (size_t)2 * w * NT;              // [RB][HP] vertical maxima -> prefix maxima
+  T* hs = hp + (size_t)RB * HP;                   // [RB][HP] suffix maxima
+  double* dred = reinterpret_cast<double*>(hs + (size_t)RB * HP);
+  const int tid = threadIdx.x;
+  const int64_t x0 = (int64_t)blockIdx.x * TC;
+  const int64_t y0 = (int64_t)blockIdx.y * band;
+  const int nout = (int)smin<int64_t>(band, H - y0);
+  const int ncols = (int)smin<int64_t>(TC, W - x0);
+  const int64_t xi = x0 - R + tid;  // this thread's input column
+  const bool colok = xi >= 0 && xi < W;
+  const int len = nout + 2 * R;     // stream length (virtual rows y0-R ..)
+
+  if (pa.fb_reset && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *pa.fb_reset = 0ull;
+  if (pa.zero_bytes) {  // fused pipeline: clear the K3 accumulator (no memset launch)
+    const int64_t n16 = (int64_t)(pa.zero_bytes / 16);
+    const int64_t nth = (int64_t)gridDim.x * gridDim.y * NT;
+    uint4* z = static_cast<uint4*>(pa.zero);
+    for (int64_t i = ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * NT + tid; i < n16; i += nth)
+      z[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+
+  double tmax = 0.0;
+  T fmn = T(INFINITY), fmx = neg_inf<T>();
+  unsigned long long bad = 0;
+
+  // The stream is padded at the top with `pad` rows of -inf so that output
+  // row 0's window closes on a group boundary: every group of G stream steps
+  // (the unrolled register prefetch unit) then stages G whole output rows,
+  // and the horizontal pass runs once per group, outside the unrolled steps.
+  const int pad = (G - (2 * R) % G) % G;
+  const int lenp = pad + len;
+  const int first_out = pad + 2 * R;  // padded step of output row 0 (a multiple of G)
+  // padded steps [tp_lo, tp_hi) are buffer rows (uniform across the CTA)
+  const int tp_lo = (int)smax<int64_t>(0, R + pad - y0);
+  const int tp_hi = (int)smin<int64_t>(lenp, H - (y0 - R - pad));
+  const T* colp = f + (colok ? xi : 0) + (y0 - R - pad) * ld;  // row of padded step 0
+  T cur[G], nxt[G];
+  // G rows of f from padded step g (in flight together); groups wholly
+  // inside the buffer rows load without per-step checks
+  auto load_group = [&](T (&dst)[G], int g) {
+    if (g >= tp_lo && g + G <= tp_hi) {
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const T v = __ldg(colp + (int64_t)(g + u) * ld);
+        dst[u] = colok ? v : neg_inf<T>();
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < G; ++u)
+        dst[u] = (colok && g + u >= tp_lo && g + u < tp_hi) ? __ldg(colp + (int64_t)(g + u) * ld)
+                                                            : neg_inf<T>();
+    }
+  };
+  load_group(cur, 0);
+  T P = neg_inf<T>();
+  int bp = 0;    // position of the step in its vertical block (tp mod w)
+  int slot = 0;  // ring slot of the step (tp mod 2w)
+  // one group of G vertical steps; OUT: every step closes an output row's
+  // window (groups from first_out on; steps past the stream end only stage
+  // rows that are not output)
+  auto vgroup = [&](auto out_tag) {
+    constexpr bool OUT = decltype(out_tag)::value;
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const T v = cur[u];
+      P = bp == 0 ? v : vmax(P, v);
+      ring[slot * NT + tid] = v;
+      if (bp == w - 1) stream_suffix(ring + (slot - (w - 1)) * NT + tid, w, NT);
+      if (OUT) {
+        // window of the output row: padded steps [tp - 2R, tp]
+        int ss = slot - 2 * R;
+        ss += ss < 0 ? 2 * w : 0;
+        hp[u * HP + tid] = bp == w - 1 ? P : vmax(ring[ss * NT + tid], P);
+      }
+      bp = bp == w - 1 ? 0 : bp + 1;
+      slot = slot == 2 * w - 1 ? 0 : slot + 1;
+    }
+  };
+  for (int g0 = 0; g0 < lenp; g0 += G) {
+    load_group(nxt, g0 + G);
+    if (g0 >= first_out)
+      vgroup(std::true_type{});
+    else
+      vgroup(std::false_type{});
+    if (g0 >= first_out) {
+      const int jb = min(G, lenp - g0);  // output rows staged by this group
+      const int jr0 = g0 - first_out;    // band-relative row of staged row 0
+      // ---- horizontal pass over the staged rows ----
+      __syncthreads();
+      const int nblk = (NT + w - 1) / w;
+      for (int it = tid; it < jb * nblk; it += NT) {
+        const int r = it % jb, b = it / jb;
+        const int n = min(w, NT - b * w);
+        stream_scan_row(hp + r * HP + b * w, hs + r * HP + b * w, n);
+      }
+      __syncthreads();
+      // outputs of the group: M, M - f (fp64), statistics -- thread per
+      // output column (ncols <= NT), the group's f samples requested first
+      if (tid < ncols) {
+        const int x = tid;
+        const T* fcol = f + x0 + x + (y0 + jr0) * ld;
+        T fo[G];
+        const int64_t yg = y0 + jr0;
+        if (jb == G && yg >= t_lo && yg + G <= t_hi) {
+#pragma unroll
+          for (int r = 0; r < G; ++r) fo[r] = __ldg(fcol + (int64_t)r * ld);
+        } else {
+#pragma unroll
+          for (int r = 0; r < G; ++r)
+            fo[r] = (r < jb && yg + r >= t_lo && yg + r < t_hi) ? __ldg(fcol + (int64_t)r * ld) : T(0);
+        }
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+          if (r >= jb) break;
+          const T m = vmax(hs[r * HP + x], hp[r * HP + x + 2 * R]);
+          const int64_t y = y0 + jr0 + r;
+          if (M_out) M_out[y * W + x0 + x] = m;
+          if (y >= t_lo && y < t_hi) {
+            const T fv = fo[r];
+            bad += isfinite(fv) ? 0 : 1;                // image.py:16
+            tmax = fmax(tmax, (double)m - (double)fv);  // maxfilter.py:61
+            fmn = fmin(fmn, fv);
+            fmx = fmax(fmx, fv);
+          }
+        }
+      }
+      __syncthreads();  // hp / hs are restaged by the next group
+    }
+#pragma unroll
+    for (int u = 0; u < G; ++u) cur[u] = nxt[u];
+  }
+
+  // block reduction of (T, min, max, #non-finite), then the global atomics
+  double dmn = (double)fmn, dmx = (double)fmx;
+  for (int o = 16; o; o >>= 1) {
+    tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+    dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
+    dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  const int lane = tid & 31, warp = tid >> 5;
+  __shared__ int s_last;
+  __shared__ sbf_plan s_plan;
+  if (lane == 0) {
+    dred[4 * warp] = tmax;
+    dred[4 * warp + 1] = dmn;
+    dred[4 * warp + 2] = dmx;
+    dred[4 * warp + 3] = __longlong_as_double((long long)bad);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int wv = 1; wv < NT / 32; ++wv) {
+      tmax = fmax(tmax, dred[4 * wv]);
+      dmn = fmin(dmn, dred[4 * wv + 1]);
+      dmx = fmax(dmx, dred[4 * wv + 2]);
+      bad += (unsigned long long)__double_as_longlong(dred[4 * wv + 3]);
+    }
+    atomicMax(&red[0], ord_bits(tmax));
+    atomicMin(&red[1], ord_bits(dmn));
+    atomicMax(&red[2], ord_bits(dmx));
+    if (bad) atomicAdd(&red[3], bad);
+    __threadfence();
+    s_last = 0;
+    if (atomicAdd(done, 1u) == gridDim.x * gridDim.y - 1) {
+      __threadfence();
+      finalize_stats(reinterpret_cast<double*>(red) - 4);
+      s_last = 1;
+    }
+  }
+  if (pa.on) {
+    __syncwarp();
+    if (warp == 0 && s_last)
+      plan_warp(lane == 0 ? (reinterpret_cast<double*>(red) - 4)[0] : 0.0, pa.sigma_r, pa.eps, pa.rule,
+                pa.log_2_over_eps, pa.plan, pa.terms, pa.cap, 0, 0, s_plan);
+  }
+}
+
+// statistics reset ahead of the one-pass K1 (programmatic dependent launch)
+__global__ void stats_init_pdl_kernel(double* stats, unsigned* done) {
+  pdl_wait();
+  pdl_trigger();
+  init_stats(stats, done);
+}
+
 // R == 0: T = 0 by definition (maxfilter.py:58-59); statistics only.
 template <typename T>
 __global__ void stats_only_kernel(const T* __restrict__ f, int64_t W, int64_t ld, int64_t t_lo,
@@ -445,6 +736,30 @@ int run(const void* fv, int64_t H, int64_t W, int64_t ld, int R, int64_t t_lo, i
     stats_only_kernel<T><<<2 * 148, 256, 0, st>>>(f, W, ld, t_lo, t_hi, static_cast<T*>(M_out), H,
                                                   red);
     SBF_CHECK_LAUNCH();
+  } else if (SBF_K1_STREAM && sizeof(T) == 4 && R <= 24 && H * W >= (int64_t)4 << 20 &&
+             stream_smem_bytes<T>(R) <= 200 * 1024) {
+    // measured on B200 (K1 alone, us): config 4 (4096^2, R=18) 189 -> 157;
+    // the two-pass kernels stay ahead on small images (config 2: 17 vs 20)
+    // and at R = 36 (config 5, one CTA per SM: 3.09 vs 3.59 ms)
+    // one pass over f (k1_stream_kernel); the statistics reset runs first
+    const size_t smem = stream_smem_bytes<T>(R);
+    SBF_CHECK_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(k1_stream_kernel<T>), smem));
+    SBF_CHECK_CUDA(launch_pdl(stats_init_pdl_kernel, dim3(1), dim3(1), 0, st, stats, done));
+    SBF_CHECK_LAUNCH();
+    const int TC = kStreamThreads - 2 * R;
+    const int64_t nstrips = (W + TC - 1) / TC;
+    const int per_sm = (int)smax<int64_t>(1, (int64_t)(227 * 1024) / (int64_t)(smem + 1024));
+    const int64_t slots = (int64_t)device_sm_count() * per_sm;
+    const int64_t nb = smax<int64_t>(1, (slots + nstrips - 1) / nstrips);  // about one wave
+    int64_t band = smax<int64_t>(smax<int64_t>(2 * R, 16), (H + nb - 1) / nb);
+    band = smin<int64_t>(band, 1024);
+    const int64_t nbands = (H + band - 1) / band;
+    SBF_REQUIRE(nbands <= 65535, SBF_ERR_UNSUPPORTED, "image too tall for the K1 grid");
+    SBF_CHECK_CUDA(launch_pdl(k1_stream_kernel<T>, dim3((unsigned)nstrips, (unsigned)nbands),
+                              dim3(kStreamThreads), smem, st, static_cast<const T*>(f), H, W, ld, R,
+                              (int)band, t_lo, t_hi, static_cast<T*>(M_out), red, done, pa));
+    SBF_CHECK_LAUNCH();
+    return SBF_OK;  // the last CTA wrote the final statistics
   } else {
     SBF_REQUIRE(ws_bytes >= (size_t)(H * W) * sizeof(T), SBF_ERR_WORKSPACE,
                 "local_range workspace too small");
