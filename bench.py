@@ -50,6 +50,7 @@ OPS_PER_PX = 10         # local range ~8 + divide ~2
 L2_FLUSH_BYTES = 256 << 20
 E2E_LANES = 4  # streams of the batch API in the e2e leg (copy engine both ways)
 PEAK_FP32_NOMINAL = 148 * 128 * 1.965e9 / 1e12  # T lane-ops/s (FADD/FMUL/FFMA = 1 op)
+DFMA_PEAK_MEASURED = 16.99  # T DFMA/s on the pool's B200 (profiles/r2_fma_probe.txt)
 DATA = "synthetic (SURVEY.md Appendix A seeded generator; BASELINE names no dataset)"
 
 
@@ -311,7 +312,7 @@ class Pipeline:
     """Device-resident sbf_shiftable_bf calls on a set of images, rotating
     over `lanes` streams (own workspace and meta block per image slot)."""
 
-    def __init__(self, torch, dev, imgs, params, lanes):
+    def __init__(self, torch, dev, imgs, params, lanes, prec=None):
         from paper_1203_5128_b200 import _lib
         from paper_1203_5128_b200.kernels import log_2_over_eps
         from paper_1203_5128_b200.spatial import to_c_spatial
@@ -322,14 +323,16 @@ class Pipeline:
         self.R = params.resolved_radius()
         self.l2e = log_2_over_eps(params.epsilon)
         self.dts = [_lib.SBF_F64 if f.dtype == torch.float64 else _lib.SBF_F32 for f in imgs]
+        # the precision the public API settles on for these images (fp32
+        # kernels; config 3's 16-bit range takes the fp64 path)
+        self.prec = _lib.PREC_FP32 if prec is None else prec
         self.outs = [torch.empty(f.shape, dtype=f.dtype, device=dev) for f in imgs]
         self.meta = torch.empty((len(imgs), 256), dtype=torch.uint8, device=dev)
         self.main = torch.cuda.current_stream()
         self.lanes = []
         for k in range(max(1, lanes)):
             H, W = imgs[0].shape
-            ws = self.lib.sbf_shiftable_bf_workspace(H, W, self.dts[0], self.sp, _lib.PREC_FP32,
-                                                     1 << 16)
+            ws = self.lib.sbf_shiftable_bf_workspace(H, W, self.dts[0], self.sp, self.prec, 1 << 16)
             self.lanes.append(dict(stream=torch.cuda.Stream(device=dev) if lanes > 1 else self.main,
                                    ws=torch.empty(ws, dtype=torch.uint8, device=dev)))
 
@@ -339,7 +342,7 @@ class Pipeline:
         m = self.meta[i].data_ptr()
         _lib.check(self.lib.sbf_shiftable_bf(
             f.data_ptr(), self.dts[i], H, W, self.sp, self.R, -1.0, p.sigma_r, p.epsilon, 0,
-            self.l2e, _lib.PREC_FP32, self.outs[i].data_ptr(), self.dts[i], m, m + 128, m + 64,
+            self.l2e, self.prec, self.outs[i].data_ptr(), self.dts[i], m, m + 128, m + 64,
             1 << 16, lane["ws"].data_ptr(), lane["ws"].numel(), lane["stream"].cuda_stream))
 
     def step(self):
@@ -403,7 +406,8 @@ def run_ours(args, rank, world, dev):
         host = [np.ascontiguousarray(config_image(cfg))]
         flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     imgs = [torch.from_numpy(a).to(dev) for a in host]
-    pipe = Pipeline(torch, dev, imgs, params, args.lanes if cfg == 4 else 1)
+    pipe = Pipeline(torch, dev, imgs, params, args.lanes if cfg == 4 else 1,
+                    prec=_lib.PREC_HDR if cfg == 3 else _lib.PREC_FP32)
     st = pipe.main
 
     for _ in range(args.warmup):
@@ -481,6 +485,40 @@ def run_ours(args, rank, world, dev):
     achieved = k3_ops / (k3_ms * 1e-3) / 1e12
     sum_k = sum(k for _, k in k3)
     step_ops = OPS_PER_PX_TERM * sum(n * k for n, (_, k) in zip(px, k3)) + OPS_PER_PX * sum(px)
+    roof = dict(
+        bound="fp32", achieved=achieved, peak=PEAK_FP32_NOMINAL, unit="TFLOP/s",
+        frac=achieved / PEAK_FP32_NOMINAL, traffic=profile_traffic(cfg),
+        peak_source="nominal 148 SM x 128 FP32 lanes x 1.965 GHz (FADD/FMUL/FFMA = 1 op); "
+                    "MEASURED_PEAKS.json has no FP32 entry",
+        peak_measured_ffma2=peak2, frac_of_measured=achieved / peak2,
+        kernel="K3 term sweep + fused epilogue, each image alone on one stream (CUDA events)",
+        ops_per_launch=k3_ops / len(k3), k3_ms_per_launch=k3_ms / len(k3),
+        ops_basis=f"{OPS_PER_PX_TERM} ops/px/evaluated term x {px[0]} px x K_eval "
+                  f"(sum over this rank's {len(k3)} image(s) = {sum_k})",
+        traffic_source=f"profiles/k3_traffic_cfg{cfg}.json (ncu --set full)")
+    if cfg == 3:
+        # untruncated 16-bit plan (M = 0): the exact dual form (fp64) runs
+        # instead of the K = 1232 term sweeps; its own roofline is fp64 issue:
+        # 3 fp64 ops per tap (weight product, num FMA, den add) over the
+        # clamped (2S+1)^2 taps, against the measured DFMA peak
+        from paper_1203_5128_b200.spatial import to_c_spatial
+        spc = to_c_spatial(params.resolved_spatial())
+        S = spc.passes * (spc.r + 1)
+        H3, W3 = imgs[0].shape
+        ny = sum(min(S, y) + min(S, H3 - 1 - y) + 1 for y in range(H3))
+        nx = sum(min(S, x) + min(S, W3 - 1 - x) + 1 for x in range(W3))
+        ops = 3.0 * ny * nx
+        ach = ops / (k3_ms / len(k3) * 1e-3) / 1e12
+        roof = dict(bound="fp64", achieved=ach, peak=DFMA_PEAK_MEASURED, unit="TFLOP/s",
+                    frac=ach / DFMA_PEAK_MEASURED, traffic=None,
+                    peak_source="DFMA probe (tools/gpu/fma_probe.cu, profiles/r2_fma_probe.txt: "
+                                "8 independent chains, 32 warps/SM), 1 op per DFMA",
+                    kernel="dual_lut_kernel (exact dual form, fp64), each image alone (CUDA events)",
+                    ops_per_launch=ops, k3_ms_per_launch=k3_ms / len(k3),
+                    ops_basis=f"3 fp64 ops/tap x {ny * nx:.4g} taps ((2S+1)^2 clamped, S={S})",
+                    shiftable_equivalent=dict(
+                        achieved=achieved, frac_of_fp32_nominal=achieved / PEAK_FP32_NOMINAL,
+                        note="132 ops/px/term x K_eval of the term sweeps it replaces"))
     return dict(
         value=value, ms_per_step=step_ms / args.steps, clocks=clk.summary(),
         launches=KERNELS_PER_IMAGE * len(imgs) * args.steps,
@@ -491,21 +529,13 @@ def run_ours(args, rank, world, dev):
                        "both PCIe directions overlap other images' kernels") if cfg == 4 else
                       ("shiftable_bf on a pinned host tensor: SM-staged H2D, K1..K3, the K3 "
                        "epilogue writes the result into pinned host memory, one host sync")),
-        roofline=dict(
-            bound="fp32", achieved=achieved, peak=PEAK_FP32_NOMINAL, unit="TFLOP/s",
-            frac=achieved / PEAK_FP32_NOMINAL, traffic=profile_traffic(cfg),
-            peak_source="nominal 148 SM x 128 FP32 lanes x 1.965 GHz (FADD/FMUL/FFMA = 1 op); "
-                        "MEASURED_PEAKS.json has no FP32 entry",
-            peak_measured_ffma2=peak2, frac_of_measured=achieved / peak2,
-            kernel="K3 term sweep + fused epilogue, each image alone on one stream (CUDA events)",
-            ops_per_launch=k3_ops / len(k3), k3_ms_per_launch=k3_ms / len(k3),
-            ops_basis=f"{OPS_PER_PX_TERM} ops/px/evaluated term x {px[0]} px x K_eval "
-                      f"(sum over this rank's {len(k3)} image(s) = {sum_k})",
-            traffic_source=f"profiles/k3_traffic_cfg{cfg}.json (ncu --set full)"),
+        roofline=roof,
         step_roofline=dict(achieved=step_ops * args.steps / (step_ms * 1e-3) / 1e12 * world,
                            frac=step_ops * args.steps / (step_ms * 1e-3) / 1e12 * world
                            / (PEAK_FP32_NOMINAL * world),
-                           note="whole step (all kernels, all ranks) against world x nominal peak"),
+                           note="whole step (all kernels, all ranks) against world x nominal peak"
+                                + ("; shiftable-equivalent ops (the dual form evaluates a different, "
+                                   "cheaper exact sum for this M = 0 plan)" if cfg == 3 else "")),
         plans=[(float(pl.T), int(pl.N), int(pl.M), int(pl.K_eval)) for pl in plans[:4]])
 
 

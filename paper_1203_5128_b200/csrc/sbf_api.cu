@@ -725,12 +725,18 @@ int launch_filter(const FilterLaunch& a) {
                                      a.stream));
       SBF_CHECK_CUDA(cudaStreamSynchronize(a.stream));
       if (g_dual_mode == 2 ? (plan.status == SBF_OK && plan.M == 0 && plan.K_eval > 0)
-                           : dual_preferred(a, plan))
-        return launch_dual_direct(a, plan);
+                           : dual_preferred(a, plan)) {
+        if (g_k3_ev[0]) SBF_CHECK_CUDA(cudaEventRecord(g_k3_ev[0], a.stream));
+        const int rc = launch_dual_direct(a, plan);
+        if (rc == SBF_OK && g_k3_ev[1]) SBF_CHECK_CUDA(cudaEventRecord(g_k3_ev[1], a.stream));
+        return rc;
+      }
     }
     double* nd = static_cast<double*>(a.ws);
+    if (g_k3_ev[0]) SBF_CHECK_CUDA(cudaEventRecord(g_k3_ev[0], a.stream));
     int rc = launch_generic_terms(a, nd);
     if (rc != SBF_OK) return rc;
+    if (g_k3_ev[1]) SBF_CHECK_CUDA(cudaEventRecord(g_k3_ev[1], a.stream));
     return launch_epilogue<double>(a, nd, 1, rows_out * a.W);
   }
   TermGeom g;

@@ -20,6 +20,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--size", type=int, default=None)
+ap.add_argument("--prec", default="fp32", choices=["fp32", "hdr", "auto"])
+ap.add_argument("--fp64-method", type=int, default=None, help="sbf_set_fp64_method (0 sweeps, 1 model, 2 dual)")
 a = ap.parse_args()
 p = CONFIGS[a.config]
 img = config_image(a.config, size=a.size)
@@ -30,7 +32,9 @@ dt = _lib.SBF_F64 if f.dtype == torch.float64 else _lib.SBF_F32
 params = P.FilterParams(sigma_s=p["sigma_s"], sigma_r=p["sigma_r"], epsilon=p["epsilon"])
 sp = to_c_spatial(params.resolved_spatial())
 R = params.resolved_radius()
-prec = _lib.PREC_FP32
+prec = {"fp32": _lib.PREC_FP32, "hdr": _lib.PREC_HDR, "auto": _lib.PREC_AUTO}[a.prec]
+if a.fp64_method is not None:
+    lib.sbf_set_fp64_method(a.fp64_method)
 cap = 1 << 16
 ws = torch.empty(lib.sbf_shiftable_bf_workspace(H, W, dt, sp, prec, cap), dtype=torch.uint8, device="cuda")
 stats = torch.empty(8, dtype=torch.float64, device="cuda")
