@@ -252,6 +252,18 @@ __device__ __forceinline__ bool sweep_needs_hdr(const double* stats) {
   return fmax(stats[2] - c, c - stats[1]) > 4096.0;
 }
 
+#ifndef SBF_SWEEP_HPF
+#define SBF_SWEEP_HPF 0  // H phase: columns read ahead (0: plain loads)
+#endif
+#ifndef SBF_SWEEP_VPF
+#define SBF_SWEEP_VPF 0  // V phase: rows of the f box read ahead (0: plain loads)
+#endif
+#ifndef SBF_SWEEP_ACC_BATCH
+#define SBF_SWEEP_ACC_BATCH 0  // accumulate: batched shared-memory reads, clobber-free reds
+#endif
+#ifndef SBF_SWEEP_ABL
+#define SBF_SWEEP_ABL 0  // phase ablation for timing studies (wrong results when != 0)
+#endif
 #ifndef SBF_SWEEP_TMA
 #define SBF_SWEEP_TMA 1  // 0: the threads load the f box themselves (debug / comparison)
 #endif
@@ -455,12 +467,34 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
         const int rs0 = base % RING;
         float* rdst = RAW + rs0 * RAWP + (q - HALO);
         const bool out_col = q >= HALO && q < HALO + WC;
+        // f of the next VPF steps is read ahead of the current step's work
+        float fr[SBF_SWEEP_VPF > 0 ? SBF_SWEEP_VPF : 1];
+#pragma unroll
+        for (int k = 0; k < SBF_SWEEP_VPF; ++k)
+          fr[k] = (KIND == 0 || (unsigned)(rel + k) < (unsigned)ROWS) ? fsrc[k * C::FCOLS] : 0.f;
         sweep_for<L>([&](auto jc) {
           constexpr int J = decltype(jc)::value;
           if (KIND != 0 && (unsigned)(rel + J) >= (unsigned)ROWS) return;
-          const float fc = fsrc[J * C::FCOLS] - fcent;
+          float fraw;
+          if (SBF_SWEEP_VPF > 0) {
+            fraw = fr[0];
+#pragma unroll
+            for (int k = 0; k + 1 < SBF_SWEEP_VPF; ++k) fr[k] = fr[k + 1];
+            constexpr int JN = J + (SBF_SWEEP_VPF > 0 ? SBF_SWEEP_VPF : 0);
+            if (JN < L)
+              fr[SBF_SWEEP_VPF > 0 ? SBF_SWEEP_VPF - 1 : 0] =
+                  (KIND == 0 || (unsigned)(rel + JN) < (unsigned)ROWS) ? fsrc[JN * C::FCOLS] : 0.f;
+          } else {
+            fraw = fsrc[J * C::FCOLS];
+          }
+          const float fc = fraw - fcent;
           float sv, cv;
+#if SBF_SWEEP_ABL & 8  // timing ablation only: no MUFU phasor in the V phase
+          cv = fc * omega;
+          sv = cv + 0.5f;
+#else
           __sincosf(fc * omega, &sv, &cv);
+#endif
           if (BORDER) {  // rows outside the image contribute nothing
             const int64_t gr = grow0 + base + J;
             const float m = (gr >= 0 && gr < p.img_H) ? 1.f : 0.f;
@@ -471,15 +505,20 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
           if (out_col) rdst[J * RAWP] = fc;
           const float* gt = gv + base + J + GOFF;
           const float2 fx = make_float2(fc, 1.f);
+#if SBF_SWEEP_ABL & 2  // timing ablation only: no V recurrences
+          const float2 ya = __fmul2_rn(fx, pk(cv)), yb = __fmul2_rn(fx, pk(sv));
+#else
           const float2 ya = vcascade<J, L, D, PASSES, BORDER>(dA, lA, __fmul2_rn(fx, pk(cv)), a2, nb2, b2, gt);
           const float2 yb = vcascade<J, L, D, PASSES, BORDER>(dB, lB, __fmul2_rn(fx, pk(sv)), a2, nb2, b2, gt);
+#endif
           // VB layout per pixel: [F_c, G_c, F_s, G_s]
           sts2(vdst + J * VBP, ya);
           sts2(vdst + J * VBP + 2, yb);
         });
       };
 #pragma unroll 1
-      for (int base = (t0 / L) * L; base < t0 + ROWS; base += L) {
+      // (steps past the band's stream end feed no output row: skipped)
+      for (int base = (t0 / L) * L; base < min(t0 + ROWS, T_total); base += L) {
         const bool clean = base - (PASSES + 2) * D - 1 >= sg_lo && base + L - 1 <= sg_hi;
         if (!clean)
           vblock(std::integral_constant<int, 2>{}, base);
@@ -508,6 +547,12 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
         for (int pp = 0; pp < PASSES; ++pp)
 #pragma unroll
           for (int j = 0; j < L; ++j) hd[pp][j] = 0.f;
+        // inputs are read HPF columns ahead (a shift register carried from
+        // block to block): the shared-memory latency overlaps the recurrences
+        // instead of opening every column step
+        float xr[SBF_SWEEP_HPF > 0 ? SBF_SWEEP_HPF : 1];
+#pragma unroll
+        for (int k = 0; k < SBF_SWEEP_HPF; ++k) xr[k] = vrow[4 * k];
         // kind: 0 warm-up (no outputs), 1 main, 2 guarded, 3 border
         auto hblock = [&](auto kind_tag, const int hbase) {
           constexpr int KIND = decltype(kind_tag)::value;
@@ -515,12 +560,25 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
           sweep_for<L>([&](auto jc) {
             constexpr int J = decltype(jc)::value;
             const int qq = hbase + J;
-            float x = vrow[4 * qq];
+            float x;
+            if (SBF_SWEEP_HPF > 0) {
+              x = xr[0];
+#pragma unroll
+              for (int k = 0; k + 1 < SBF_SWEEP_HPF; ++k) xr[k] = xr[k + 1];
+              const int qn = qq + SBF_SWEEP_HPF;
+              xr[SBF_SWEEP_HPF > 0 ? SBF_SWEEP_HPF - 1 : 0] = qn < C::VB_COLS ? vrow[4 * qn] : 0.f;
+            } else {
+              x = vrow[4 * qq];
+            }
             if (BORDER) {
               const int cc = xs + qq;
               x = (cc >= 0 && cc < p.W) ? x : 0.f;
             }
+#if SBF_SWEEP_ABL & 1  // timing ablation only: no H recurrences
+            const float yv = x * a;
+#else
             const float yv = hcascade<J, L, D, PASSES, BORDER>(hd, hlast, x, a, b, gh + qq + GOFF);
+#endif
             if (KIND == 1 || (GUARD && qq >= 2 * HALO && qq < COLS)) vrow[4 * (qq - HALO)] = yv;
           });
         };
@@ -573,19 +631,59 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
           int slot = (t0 + vlo - HALO) % RING;
           const float* rp = RAW + jc;
           const float2 fx = make_float2(scale * nscale, scale * dscale);
+#if SBF_SWEEP_ACC_BATCH
+          // 4 pixels' shared-memory reads issued before any is consumed; the
+          // reds carry no memory clobber (the chunk's __syncthreads orders them)
+          for (int v0 = 0; v0 < nr; v0 += 4) {
+            float4 pvb[4];
+            float fcb[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (v0 + u < nr) {
+                pvb[u] = *reinterpret_cast<const float4*>(vb + (v0 + u) * VBP);
+                fcb[u] = rp[slot * RAWP];
+                slot = slot + 1 == RING ? 0 : slot + 1;
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (v0 + u >= nr) break;
+              const float4 pv = pvb[u];
+              const float fcv = fcb[u];
+              float sv, cv;
+              __sincosf(fcv * omega, &sv, &cv);
+              float2 t = __ffma2_rn(pk(sv), make_float2(pv.z, pv.w),
+                                    __fmul2_rn(pk(cv), make_float2(pv.x, pv.y)));
+              t = __fmul2_rn(t, fx);
+              const long long q =
+                  ((long long)__float2int_rn(t.x) << 32) + (long long)__float2int_rn(t.y);
+              asm volatile("red.global.add.u64 [%0], %1;" ::"l"(dst + (int64_t)(v0 + u) * p.W), "l"(q));
+            }
+          }
+#else
 #pragma unroll 4
           for (int v = 0; v < nr; ++v) {
             const float4 pv = *reinterpret_cast<const float4*>(vb + v * VBP);
             const float fcv = rp[slot * RAWP];
             slot = slot + 1 == RING ? 0 : slot + 1;
             float sv, cv;
+#if SBF_SWEEP_ABL & 16  // timing ablation only: no MUFU phasor in the accumulate phase
+            cv = fcv * omega;
+            sv = cv + 0.5f;
+#else
             __sincosf(fcv * omega, &sv, &cv);
+#endif
             float2 t = __ffma2_rn(pk(sv), make_float2(pv.z, pv.w),
                                   __fmul2_rn(pk(cv), make_float2(pv.x, pv.y)));
             t = __fmul2_rn(t, fx);
             const long long q = ((long long)__float2int_rn(t.x) << 32) + (long long)__float2int_rn(t.y);
+#if SBF_SWEEP_ABL & 4  // timing ablation only: no accumulation atomics
+            if (q == 0x7fffffffffffll) dst[(int64_t)v * p.W] = q;
+#else
             asm volatile("red.global.add.u64 [%0], %1;" ::"l"(dst + (int64_t)v * p.W), "l"(q) : "memory");
+#endif
           }
+#endif
         }
       }
       __syncthreads();  // VB / RAW are rewritten by the next chunk
@@ -593,19 +691,21 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
     // this item's rows are in: count it on the output segments it covers;
     // the item that completes a segment (all terms, all bands over it)
     // divides it out (bilateral.py:242-254) and writes the output
+    // (one segment counter per thread: the round trips to L2 overlap
+    // instead of running one after another in one thread)
     __threadfence();
+    if (tid == 0) s_ndone = 0;
     __syncthreads();
-    if (tid == 0) {
-      int n = 0;
+    {
       const int s0 = (y0 - p.out_lo) / SEGR, s1 = (y1 - 1 - p.out_lo) / SEGR;
-      for (int sg = s0; sg <= s1; ++sg) {
+      for (int sg = s0 + tid; sg <= s1; sg += THREADS) {
         const int r0 = sg * SEGR, r1 = min(rows_all, r0 + SEGR) - 1;
         const int nm = r1 / bandh - r0 / bandh + 1;
         const int nt = Ks > 0 ? r1 / bandh_s - r0 / bandh_s + 1 : 0;
         const int expected = (K_eval - Ks) * nm + Ks * nt;
-        if (atomicAdd(p.seg + (int64_t)sg * p.nstrips + strip, 1) == expected - 1) s_done[n++] = sg;
+        if (atomicAdd(p.seg + (int64_t)sg * p.nstrips + strip, 1) == expected - 1)
+          s_done[atomicAdd(&s_ndone, 1)] = sg;
       }
-      s_ndone = n;
       __threadfence();
     }
     __syncthreads();
