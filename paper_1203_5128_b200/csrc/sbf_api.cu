@@ -218,7 +218,9 @@ static size_t sweep_ws(const SweepEntry& w, int64_t H, int64_t W, int64_t rows_o
 }
 
 static size_t split_ws_core(int64_t H, int64_t W, int64_t rows_out, int dtype) {
-  size_t bytes = align_up((size_t)(rows_out * W) * 8) + align_up((size_t)(rows_out * W) * 16);
+  // (num, den), SBF_SPLIT_TPI U slots (the terms of one SH item), fp32 view of fp64 inputs
+  size_t bytes = align_up((size_t)(rows_out * W) * 8) +
+                 (size_t)SBF_SPLIT_TPI * align_up((size_t)(rows_out * W) * 16);
   if (dtype == SBF_F64) bytes += align_up((size_t)(H * W) * 4);
   return bytes;
 }
@@ -490,7 +492,7 @@ static const float* f32_view(const FilterLaunch& a, void* scratch, int64_t* ld, 
 static int launch_split_path(const FilterLaunch& a, const SplitEntry& se, int r, double alpha) {
   const int64_t rows_out = a.out_hi - a.out_lo;
   const size_t nd_bytes = align_up((size_t)(rows_out * a.W) * 8);
-  const size_t u_bytes = align_up((size_t)(rows_out * a.W) * 16);
+  const size_t u_bytes = (size_t)SBF_SPLIT_TPI * align_up((size_t)(rows_out * a.W) * 16);  // U slots
   const size_t need = filter_ws(a.H, a.W, rows_out, a.dtype, &a.sp, a.precision);
   SBF_REQUIRE(a.ws && a.ws_bytes >= need, SBF_ERR_WORKSPACE,
               "filter workspace too small (%zu < %zu)", a.ws_bytes, need);
@@ -514,6 +516,7 @@ static int launch_split_path(const FilterLaunch& a, const SplitEntry& se, int r,
   p.stats = a.stats;
   p.nd = reinterpret_cast<float2*>(ws);
   p.U = reinterpret_cast<float*>(ws + nd_bytes);
+  p.u_slot = (int64_t)(align_up((size_t)(rows_out * a.W) * 16) / 4);
   // geometry: >= 4 CTAs per SM for both kernels, halos <= 1/8 of the work
   const int halo = se.passes * (r + 1);
   const int64_t sv_cols = (r <= 4) ? 128 : 64;
@@ -522,7 +525,7 @@ static int launch_split_path(const FilterLaunch& a, const SplitEntry& se, int r,
   const int64_t nb = smax<int64_t>(1, (want + cgroups - 1) / cgroups);
   p.band = (int)smin<int64_t>(smax<int64_t>(8 * halo, (rows_out + nb - 1) / nb), 1024);
   p.band = (p.band + 31) / 32 * 32;  // whole SH row groups per band
-  const int64_t rgroups = (rows_out + 31) / 32;
+  const int64_t rgroups = (rows_out + se.sh_rows - 1) / se.sh_rows;
   const int64_t ns = smax<int64_t>(1, (want + rgroups - 1) / rgroups);
   p.seg = (int)smax<int64_t>(16 * halo, (a.W + ns - 1) / ns);
   p.svx = (int)cgroups;

@@ -29,10 +29,10 @@ struct SplitParams {
   const sbf_plan* plan;
   const sbf_term* terms;
   const double* stats;
-  float* U;    // [rows_out][W][4] column-smoothed images of the current term
+  float* U;    // SBF_SPLIT_TPI slots of [rows_out][W][4] column-smoothed images (term k in slot k % TPI)
+  int64_t u_slot;  // floats from one slot to the next
   float2* nd;  // [rows_out][W] (num, den)
   int term;
-  int first;
   int band;  // SV output rows per CTA (a multiple of SH_ROWS)
   int seg;   // SH output columns per CTA
   int hdr_guard;  // SBF_PREC_AUTO: flag the plan and do nothing on wide ranges
@@ -43,6 +43,10 @@ struct SplitParams {
   int svx, svy, shx, shy;
 };
 
+#ifndef SBF_SPLIT_TPI
+#define SBF_SPLIT_TPI 2  // consecutive terms per SH item (U slots in flight)
+#endif
+
 template <int R, int PASSES>
 struct SplitCfg {
   static constexpr int D = R + 1;
@@ -52,8 +56,12 @@ struct SplitCfg {
   static constexpr int SV_COLS = (IMGS == 4) ? 128 : 64;
   static constexpr int SV_THREADS = SV_COLS * 4 / IMGS;
   static constexpr int GOFF = (PASSES + 2) * D + 2;
-  // SH: 32 rows x 4 images = 128 lanes; tile = 2L stream positions, ring of 3
-  static constexpr int SH_ROWS = 32;
+  // SH: TPI consecutive terms per item; (32 / TPI) rows x 4 images x TPI
+  // terms = 128 lanes (one recurrence each); tile = 2L stream positions,
+  // ring of 3
+  static constexpr int TPI = SBF_SPLIT_TPI;
+  static_assert(TPI == 1 || TPI == 2 || TPI == 4, "128 SH lanes");
+  static constexpr int SH_ROWS = 32 / TPI;
   static constexpr int SH_THREADS = 128;
   static constexpr int TILE = 2 * L;
   static constexpr int NTILE = 3;
@@ -102,7 +110,8 @@ __device__ __forceinline__ void sv_tile(const SplitParams& p, const int bx, cons
   const bool colok = col < p.W;
   const int colc = colok ? col : p.W - 1;
   const float* fcol = p.f + (int64_t)(y0 - HALO) * p.ld + colc;
-  float* urow = p.U + ((int64_t)(y0 - p.out_lo - 2 * HALO) * p.W + col) * 4 + 2 * pair;
+  float* urow = p.U + (int64_t)(p.term % C::TPI) * p.u_slot +
+               ((int64_t)(y0 - p.out_lo - 2 * HALO) * p.W + col) * 4 + 2 * pair;
 
   VState<R, PASSES> st;
 #pragma unroll
@@ -188,20 +197,25 @@ __device__ __forceinline__ void sv_tile(const SplitParams& p, const int bx, cons
 
 // ============================ SH: row sweep ==============================
 // Stream position s = input column + HALO; the output of step s is column
-// s - 2*HALO.  A CTA owns 32 rows and the output columns [c0, c0 + seg): it
-// streams s in [c0, c0 + seg + 2*HALO) from a zero state (exact: outputs at
-// columns >= c0 depend only on inputs >= c0 - HALO).  The ring holds stream
-// positions mod RINGC relative to the segment start; an output replaces its
-// own input (position s - HALO) in place.
+// s - 2*HALO.  A CTA owns SH_ROWS rows and the output columns [c0, c0 + seg)
+// for TPI consecutive terms kA, kA + 1, ...: lane (t, row, image) streams
+// term kA + t's image of that row from U slot t, from a zero state
+// (exact: outputs at columns >= c0 depend only on inputs >= c0 - HALO).  The
+// ring holds stream positions mod RINGC relative to the segment start; an
+// output replaces its own input (position s - HALO) in place.  Both terms'
+// contributions are added to (num, den) in one read-modify-write, and the
+// output pixels' f samples are read once for the pair.
 template <int R, int PASSES>
-__device__ __forceinline__ void sh_tile(const SplitParams& p, const int bx, const int by) {
+__device__ __forceinline__ void sh_tile(const SplitParams& p, const int bx, const int by,
+                                        const int kA, const int nterms) {
   using C = SplitCfg<R, PASSES>;
   constexpr int D = C::D, L = C::L, HALO = C::HALO, IMGS = C::IMGS, GOFF = C::GOFF;
   constexpr int TILE = C::TILE, NTILE = C::NTILE, RINGC = C::RINGC, RP = C::RPITCH;
-  constexpr int ROWS = C::SH_ROWS, GE = C::GEDGE;
+  constexpr int ROWS = C::SH_ROWS, GE = C::GEDGE, TPI = C::TPI;
+  static_assert(IMGS == 2, "the U / ring order below is [F_c, G_c, F_s, G_s]");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float* ring = reinterpret_cast<float*>(smem_raw);  // [ROWS][RPITCH]
-  float* gL = ring + ROWS * RP;                     // factors at stream positions [s0 - GOFF, s0 + GE)
+  float* ring = reinterpret_cast<float*>(smem_raw);  // [TPI][ROWS][RPITCH]
+  float* gL = ring + TPI * ROWS * RP;               // factors at stream positions [s0 - GOFF, s0 + GE)
   float* gR = gL + GE + GOFF;                       // factors at [sR0 - GOFF, sR0 + GE + GOFF)
 
   const int tid = threadIdx.x;
@@ -215,9 +229,13 @@ __device__ __forceinline__ void sh_tile(const SplitParams& p, const int bx, cons
     gR[k] = gfactor((int64_t)(sR0 + k - GOFF) - HALO, W, p.r, p.alpha);
   }
   const float a = p.a, b = p.b;
-  const sbf_term term = p.terms[p.term];
-  const float scale = (float)term.scale;
-  const float nu = (float)term.turns;
+  float scale[TPI], nu[TPI];
+#pragma unroll
+  for (int t = 0; t < TPI; ++t) {
+    const sbf_term term = p.terms[t < nterms ? kA + t : kA];
+    scale[t] = t < nterms ? (float)term.scale : 0.f;
+    nu[t] = (float)term.turns;
+  }
   const float centerf = p.centred ? 0.f : (float)p.stats[3];
   const int r0 = p.out_lo + bx * ROWS;  // first buffer row of this CTA
   const int nrows = min(ROWS, p.out_hi - r0);
@@ -227,15 +245,15 @@ __device__ __forceinline__ void sh_tile(const SplitParams& p, const int bx, cons
   const int ntiles = (s1 - s0 + TILE - 1) / TILE;
   auto load_tile = [&](int j) {
     const int slot = (j % NTILE) * TILE;
-    for (int k = tid; k < ROWS * TILE; k += 128) {
-      const int rr = k / TILE, cc = k - rr * TILE;
+    for (int k = tid; k < TPI * ROWS * TILE; k += 128) {
+      const int t = k / (ROWS * TILE), k2 = k - t * (ROWS * TILE);
+      const int rr = k2 / TILE, cc = k2 - rr * TILE;
       const int c = s0 + j * TILE + cc - HALO;
-      float* dst = ring + rr * RP + 4 * (slot + cc);
-      if (rr < nrows && c >= 0 && c < W) {
+      float* dst = ring + (t * ROWS + rr) * RP + 4 * (slot + cc);
+      if (t < nterms && rr < nrows && c >= 0 && c < W) {
+        const float* src = Ub + (int64_t)t * p.u_slot + ((int64_t)rr * W + c) * 4;  // term kA + t
         const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d),
-                     "l"(Ub + ((int64_t)rr * W + c) * 4)
-                     : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
       } else {
         *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
       }
@@ -245,14 +263,16 @@ __device__ __forceinline__ void sh_tile(const SplitParams& p, const int bx, cons
   load_tile(0);
   if (ntiles > 1) load_tile(1);
 
-  const int hv = tid >> 2, himg = tid & 3;
+  const int ht = tid / (4 * ROWS);             // term of this H lane
+  const int hv = (tid >> 2) % ROWS, himg = tid & 3;
   float hd[PASSES][L];
   float hlast = 0.f;
 #pragma unroll
   for (int pp = 0; pp < PASSES; ++pp)
 #pragma unroll
     for (int j = 0; j < L; ++j) hd[pp][j] = 0.f;
-  float* lrow = ring + hv * RP + himg;
+  float* lrow = ring + (ht * ROWS + hv) * RP + himg;
+  const bool hlane = hv < nrows && ht < nterms;
   // stream positions whose reach has factor 1 (cf. K3's qg_lo / qg_hi)
   const int qg_lo = D + HALO, qg_hi = W - 1 - D + HALO;
 
@@ -301,8 +321,8 @@ __device__ __forceinline__ void sh_tile(const SplitParams& p, const int bx, cons
         const int c = s_lo + cc - 2 * HALO;
         const int64_t row = r0 + rr;
         fpx[i] = __ldg(p.f + row * p.ld + c);
-        // (num, den) of the previous term, written by another CTA: from L2
-        if (!p.first) acc_old[i] = __ldcg(p.nd + (row - p.out_lo) * W + c);
+        // (num, den) of the previous terms, written by another CTA: from L2
+        if (kA > 0) acc_old[i] = __ldcg(p.nd + (row - p.out_lo) * W + c);
       }
     }
     if (j + 1 < ntiles)
@@ -311,7 +331,7 @@ __device__ __forceinline__ void sh_tile(const SplitParams& p, const int bx, cons
       cp_async_wait<0>();
     __syncthreads();
     // ---- H phase over this tile's blocks ----
-    if (hv < nrows) {
+    if (hlane) {
 #pragma unroll 1
       for (int kb = 0; kb < TILE / L; ++kb) {
         const int base = s0 + j * TILE + kb * L;
@@ -331,7 +351,7 @@ __device__ __forceinline__ void sh_tile(const SplitParams& p, const int bx, cons
       }
     }
     __syncthreads();
-    // ---- accumulate the outputs produced in this tile ----
+    // ---- accumulate the outputs produced in this tile (both terms) ----
 #pragma unroll
     for (int i = 0; i < PX; ++i) {
       const int k = tid + i * 128;
@@ -340,16 +360,21 @@ __device__ __forceinline__ void sh_tile(const SplitParams& p, const int bx, cons
       const int s = s_lo + cc;
       const int c = s - 2 * HALO;  // output column
       const int o = (s - s0 - HALO) % RINGC;
-      const float4 v = *reinterpret_cast<const float4*>(ring + rr * RP + 4 * o);
       const float fc = fpx[i] - centerf;
-      const float u = fc * nu;
-      const float tt = u - ((u + 12582912.f) - 12582912.f);
-      float cv, sv;
-      __sincosf(tt * 6.28318530717958647f, &sv, &cv);
-      // U / ring order: IMGS==4 [F_c, F_s, G_c, G_s]; IMGS==2 [F_c, G_c, F_s, G_s]
-      const float num = scale * ((IMGS == 4) ? cv * v.x + sv * v.y : cv * v.x + sv * v.z);
-      const float den = scale * ((IMGS == 4) ? cv * v.z + sv * v.w : cv * v.y + sv * v.w);
-      p.nd[(r0 + rr - p.out_lo) * W + c] = make_float2(acc_old[i].x + num, acc_old[i].y + den);
+      float num = acc_old[i].x, den = acc_old[i].y;
+#pragma unroll
+      for (int t = 0; t < TPI; ++t) {
+        if (t >= nterms) break;
+        // ring order [F_c, G_c, F_s, G_s]
+        const float4 v = *reinterpret_cast<const float4*>(ring + (t * ROWS + rr) * RP + 4 * o);
+        const float u = fc * nu[t];
+        const float tt = u - ((u + 12582912.f) - 12582912.f);
+        float cv, sv;
+        __sincosf(tt * 6.28318530717958647f, &sv, &cv);
+        num += scale[t] * (cv * v.x + sv * v.z);
+        den += scale[t] * (cv * v.y + sv * v.w);
+      }
+      p.nd[(r0 + rr - p.out_lo) * W + c] = make_float2(num, den);
     }
     __syncthreads();
     if (j + 2 < ntiles) load_tile(j + 2);
@@ -365,7 +390,7 @@ size_t sv_smem_bytes(int band) {
 template <int R, int PASSES>
 size_t sh_smem_bytes() {
   using C = SplitCfg<R, PASSES>;
-  return (size_t)C::SH_ROWS * C::RPITCH * 4 + (size_t)2 * (C::GEDGE + C::GOFF) * 4 + 16;
+  return (size_t)C::TPI * C::SH_ROWS * C::RPITCH * 4 + (size_t)2 * (C::GEDGE + C::GOFF) * 4 + 16;
 }
 
 __device__ __forceinline__ void split_wait(const int* ctr, int target) {
@@ -381,15 +406,19 @@ __device__ __forceinline__ void split_wait(const int* ctr, int target) {
 }
 
 // Every term in one persistent launch with a device work queue: items are
-// taken in order [SV tiles of term 0 | SH tiles of term 0 | SV tiles of term
-// 1 | ...], the term count is read from the device plan (no host round
-// trip; graph-capturable).  Dependencies are per row band and only ever on
-// items taken earlier, so the queue cannot deadlock:
-//  * SH(k) tiles of band b wait for all SV(k) tiles of band b (U is complete)
-//    and for all SH(k-1) tiles of band b ((num, den) updated in term order:
-//    one owner per pixel and term, a fixed sum order);
-//  * SV(k) tiles of band b wait for all SH(k-1) tiles of band b (U, written
-//    once per term, has been consumed).
+// taken in order, per pair of terms (2j, 2j+1):
+//   [SV tiles of term 2j | SV tiles of term 2j+1 | SH tiles of the pair]
+// and the term count is read from the device plan (no host round trip;
+// graph-capturable).  Term k's column-smoothed images go to U slot k % TPI.
+// Dependencies are per row band and only ever on items taken earlier, so the
+// queue cannot deadlock:
+//  * SH(pair j) tiles of band b wait for all SV tiles of both terms of band b
+//    (U complete) and for all SH(pair j-1) tiles of band b ((num, den)
+//    updated in term order: one owner per pixel and pair, a fixed sum order);
+//  * SV(2j), SV(2j+1) tiles of band b wait for all SH(pair j-1) tiles of band
+//    b (their U slots have been consumed).
+// (An odd K leaves the last pair with one term; its second SV block only
+// counts.)
 template <int R, int PASSES>
 __global__ void __launch_bounds__(128) split_queue_kernel(SplitParams p) {
   using C = SplitCfg<R, PASSES>;
@@ -411,9 +440,11 @@ __global__ void __launch_bounds__(128) split_queue_kernel(SplitParams p) {
       p.nd[i] = make_float2(0.f, 0.f);
     return;
   }
+  constexpr int TPI = C::TPI;
+  const int npairs = (K + TPI - 1) / TPI;
   const int n_sv = p.svx * p.svy, n_sh = p.shx * p.shy;
-  const int per = n_sv + n_sh;
-  const long long total = (long long)K * per;
+  const int per = TPI * n_sv + n_sh;
+  const long long total = (long long)npairs * per;
   const int gpb = p.band / C::SH_ROWS;  // SH row groups per band
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(p.head, 1);
@@ -421,27 +452,32 @@ __global__ void __launch_bounds__(128) split_queue_kernel(SplitParams p) {
     const long long item = s_item;
     __syncthreads();  // s_item is rewritten by the next pull
     if (item >= total) break;
-    const int k = (int)(item / per), j = (int)(item - (long long)k * per);
-    p.term = k;
-    p.first = k == 0;
-    if (j < n_sv) {
-      const int bx = j % p.svx, band = j / p.svx;
+    const int pr = (int)(item / per), j = (int)(item - (long long)pr * per);
+    if (j < TPI * n_sv) {
+      const int k = pr * TPI + j / n_sv, jj = j % n_sv;
+      const int bx = jj % p.svx, band = jj / p.svx;
       const int rows_b = min(p.band, rows_out - band * p.band);
       const int nsh_b = ((rows_b + C::SH_ROWS - 1) / C::SH_ROWS) * p.shy;
-      if (k > 0) split_wait(p.sh_done + band, k * nsh_b);
-      sv_tile<R, PASSES>(p, bx, band);
-      __threadfence();
-      __syncthreads();
+      // (the missing second term of an odd K only counts -- but only once the
+      // previous pair's SH tiles are done: the counter is cumulative, so an
+      // early count could stand in for a previous pair's unfinished SV tile)
+      if (pr > 0) split_wait(p.sh_done + band, pr * nsh_b);
+      if (k < K) {
+        p.term = k;
+        sv_tile<R, PASSES>(p, bx, band);
+        __threadfence();
+        __syncthreads();
+      }
       if (threadIdx.x == 0) atomicAdd(p.sv_done + band, 1);
     } else {
-      const int jj = j - n_sv;
+      const int jj = j - TPI * n_sv;
       const int rx = jj / p.shy, sy = jj - rx * p.shy;
       const int band = rx / gpb;
       const int rows_b = min(p.band, rows_out - band * p.band);
       const int nsh_b = ((rows_b + C::SH_ROWS - 1) / C::SH_ROWS) * p.shy;
-      split_wait(p.sv_done + band, (k + 1) * p.svx);
-      if (k > 0) split_wait(p.sh_done + band, k * nsh_b);
-      sh_tile<R, PASSES>(p, rx, sy);
+      split_wait(p.sv_done + band, (pr + 1) * TPI * p.svx);
+      if (pr > 0) split_wait(p.sh_done + band, pr * nsh_b);
+      sh_tile<R, PASSES>(p, rx, sy, pr * TPI, min(TPI, K - pr * TPI));
       __threadfence();
       __syncthreads();
       if (threadIdx.x == 0) atomicAdd(p.sh_done + band, 1);
@@ -467,9 +503,10 @@ int launch_split(const SplitParams& p, cudaStream_t st) {
 struct SplitEntry {
   int r, passes;
   int (*launch)(const SplitParams&, cudaStream_t);
+  int sh_rows;  // rows per SH item
 };
 
 #define SBF_SPLIT_ENTRY(R, P) \
-  SplitEntry { R, P, &launch_split<R, P> }
+  SplitEntry { R, P, &launch_split<R, P>, SplitCfg<R, P>::SH_ROWS }
 
 }  // namespace sbf

@@ -394,3 +394,26 @@ def test_k3_event_hook_brackets_the_term_kernel():
     assert k1 > 0 and k3 > 0 and k4 >= 0 and k3 > k4
     ref = P.shiftable_bf(f, params).image
     assert float((out - ref).abs().max()) <= 1e-3
+
+
+@pytest.mark.parametrize("w,sr", [(1, 20.0), (5, 45.0), (33, 45.0), (2, 20.0)])
+def test_split_sweep_paired_terms_odd_count(w, sr):
+    """The split sweep's SH items take two terms; with an odd term count the
+    last pair has one.  Narrow images make the SV items short, which is where
+    a missing-term count once raced ahead of the previous pair's SV items:
+    five calls must agree bit for bit and match the C oracle."""
+    import torch
+    from oracle import coracle as CO
+    img = np.random.default_rng(w).uniform(0, 255, (196, w))
+    params = P.FilterParams(sigma_s=9.7, sigma_r=sr, epsilon=0.0)
+    ref = CO.shiftable_bf(img, 9.7, sr, 0.0)
+    dev = torch.from_numpy(img).cuda()
+    first = None
+    for _ in range(5):
+        res = P.shiftable_bf(dev, params)
+        assert (res.plan.N // 2 - res.plan.M + 1) % 2 == 1  # odd K
+        if first is None:
+            first = res.image.clone()
+        assert torch.equal(res.image, first)
+    d = np.abs(first.cpu().numpy() - ref["image"])
+    assert float(d.max()) <= 1e-2 and float(np.sqrt(np.mean(d * d))) <= 1e-3
