@@ -648,10 +648,31 @@ static int launch_sweep_path(const FilterLaunch& a, const SweepEntry& w, int r, 
                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   SBF_REQUIRE(cr == CUDA_SUCCESS, SBF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  // the divide/fallback epilogue: fused into the sweep (segment by segment,
+  // as items complete) when the output is page-locked host memory, so its
+  // PCIe writes overlap the sweep; a full-width kernel after the sweep for
+  // device outputs (sbf_set_fused_epilogue: 1 default, 2 always, 0 never)
+  bool out_host = false;
+  if (g_fused_epi == 1) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, a.out) == cudaSuccess)
+      out_host = at.type == cudaMemoryTypeHost;
+    else
+      cudaGetLastError();
+  }
+  p.fused_epi = (g_fused_epi == 2 || out_host) ? 1 : 0;
   if (!(g_stage_mask & 1)) return SBF_OK;
   if (g_k3_ev[0]) SBF_CHECK_CUDA(cudaEventRecord(g_k3_ev[0], a.stream));
   int rc = w.launch(map, p, a.stream);
   if (rc != SBF_OK) return rc;
+  if (!p.fused_epi) {
+    const int64_t n = rows_out * a.W;
+    const unsigned grid = (unsigned)smin<int64_t>((n + 255) / 256, (int64_t)device_sm_count() * 8);
+    SBF_CHECK_CUDA(launch_pdl(sweep_divide_kernel, dim3(grid), dim3(256), 0, a.stream,
+                              static_cast<const unsigned long long*>(p.acc), n, a.W, a.out_lo, a.f,
+                              a.ld, a.dtype, a.out, a.out_dtype, a.plan, a.stats, a.fallback));
+    SBF_CHECK_LAUNCH();
+  }
   if (g_k3_ev[1]) SBF_CHECK_CUDA(cudaEventRecord(g_k3_ev[1], a.stream));
   return SBF_OK;
 }

@@ -77,6 +77,7 @@ struct SweepParams {
   const double* stats;
   unsigned long long* fallback;
   int hdr_guard;  // SBF_PREC_AUTO: bail out (flag the plan) on wide ranges
+  int fused_epi;  // 1: the item completing a segment divides it out; 0: sweep_divide_kernel follows
 };
 
 template <int R, int PASSES>
@@ -321,6 +322,7 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
   const float nscale = ldexpf(1.f, 29 - nexp), dscale = ldexpf(1.f, 29);
   const double inv_nscale = ldexp(1.0, nexp - 29), inv_dscale = ldexp(1.0, -29);
   if (K_eval <= 0) {
+    if (!p.fused_epi) return;  // the divide kernel finds den = 0 everywhere
     // no retained term: every normaliser is 0, so every pixel falls back
     unsigned long long n = 0;
     const int64_t total = (int64_t)rows_all * p.W;
@@ -693,6 +695,10 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
     // divides it out (bilateral.py:242-254) and writes the output
     // (one segment counter per thread: the round trips to L2 overlap
     // instead of running one after another in one thread)
+    if (!p.fused_epi) {
+      __syncthreads();  // tables and VB are rewritten by the next item
+      continue;
+    }
     __threadfence();
     if (tid == 0) s_ndone = 0;
     __syncthreads();
@@ -762,6 +768,56 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
     }
     __syncthreads();  // tables, VB and the segment list are rewritten by the next item
   }  // work queue
+}
+
+// Divide / fallback epilogue for the fixed-point accumulator
+// (bilateral.py:242-254), launched after the sweep for device outputs: every
+// pixel at full GPU width, instead of one CTA per completed segment inside
+// the sweep's last items (which serialised the tail: 0.23 ms of a 2.0 ms
+// config-4 sweep).  Same decode and arithmetic as the fused epilogue.
+static __global__ void __launch_bounds__(256) sweep_divide_kernel(
+    const unsigned long long* __restrict__ acc, int64_t n, int64_t W, int64_t out_lo,
+    const void* __restrict__ fo, int64_t fo_ld, int fo_dtype, void* __restrict__ out, int out_dtype,
+    const sbf_plan* __restrict__ plan, const double* __restrict__ stats,
+    unsigned long long* __restrict__ fallback) {
+  pdl_wait();
+  if (plan->status != SBF_OK || (plan->flags & SBF_PLAN_NEEDS_HDR)) return;
+  const double centerd = stats[3];
+  const float centerf = (float)centerd;
+  const double maxdev = fmax(stats[2] - centerd, centerd - stats[1]);
+  const int nexp = ilogb(fmax(maxdev, 1.0)) + 1;
+  const double inv_nscale = ldexp(1.0, nexp - 29), inv_dscale = ldexp(1.0, -29);
+  unsigned long long bad = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const long long sum = (long long)__ldcs(acc + i);
+    const int lo = (int)(unsigned)(sum & 0xffffffffll);
+    const long long hi = (sum - (long long)lo) >> 32;
+    const double num = (double)hi * inv_nscale, den = (double)lo * inv_dscale;
+    const bool is_bad = !(den > 0.0);  // bilateral.py:244
+    bad += is_bad ? 1 : 0;
+    const int64_t y = i / W, x = i - y * W;
+    const int64_t fi = (out_lo + y) * fo_ld + x;
+    if (out_dtype == SBF_F32) {
+      float o;
+      if (is_bad)
+        o = fo_dtype == SBF_F32 ? static_cast<const float*>(fo)[fi]
+                                : (float)static_cast<const double*>(fo)[fi];
+      else
+        o = (float)(num / den) + centerf;
+      static_cast<float*>(out)[i] = o;
+    } else {
+      double o;
+      if (is_bad)
+        o = fo_dtype == SBF_F32 ? (double)static_cast<const float*>(fo)[fi]
+                                : static_cast<const double*>(fo)[fi];
+      else
+        o = num / den + centerd;
+      static_cast<double*>(out)[i] = o;
+    }
+  }
+  for (int o = 16; o; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(fallback, bad);
 }
 
 // ---- host side ----
