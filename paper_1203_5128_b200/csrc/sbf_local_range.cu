@@ -30,6 +30,12 @@ constexpr int kRowSeg = 1024;   // outputs per row-pass CTA
 #ifndef SBF_K1_VH_COL
 #define SBF_K1_VH_COL 1
 #endif
+#ifndef SBF_K1_PRUNE
+#define SBF_K1_PRUNE 1  // T by tile bounds + exact evaluation of the tiles that can raise it
+#endif
+#ifndef SBF_K1P_DBG
+#define SBF_K1P_DBG 0  // timing studies only: 1 = exact rounds select nothing, 2 = no exact rounds
+#endif
 #ifndef SBF_K1_STREAM
 #define SBF_K1_STREAM 1  // one-pass K1 (k1_stream_kernel) where the radius allows
 #endif
@@ -673,6 +679,322 @@ __global__ void stats_init_pdl_kernel(double* stats, unsigned* done) {
   init_stats(stats, done);
 }
 
+// ---------------------------------------------------------------------------
+// Pruned K1 (T only, no M image): exact, f read from HBM about once.
+//
+// T = max_x (M(x) - f(x)) with M the clamped (2R+1)^2 window maximum
+// (maxfilter.py:56-61).  For 32x32 tiles, M(x) <= max over the tiles within
+// n = ceil(R/32) tile steps of their maxima, and f(x) >= the tile's minimum,
+// so U_t = double(that max) - double(tile min) bounds the contribution of
+// every pixel of tile t (double subtraction is monotone).  Kernels:
+//   tiles   one pass over f: per-tile max (all buffer rows) and min (rows in
+//           [t_lo, t_hi)), the image statistics, the K3 accumulator clear;
+//   bounds  U_t per tile, their maximum Umax;
+//   exact 1 tiles with U_t == Umax: M - f evaluated exactly (separable window
+//           maximum in shared memory, doubling ladder), T = max;
+//   exact 2 tiles with T < U_t < Umax, the same; the last CTA finalises the
+//           statistics and builds the plan (fused pipeline).
+// Tiles whose bound cannot exceed the T already found are never evaluated:
+// on the configs' 8-bit images most tiles drop out after round 1.  The
+// result equals the full evaluation bit for bit (the max of the same fp64
+// differences).
+constexpr int kPruneTile = 32;
+constexpr int kPruneSub = 16;   // bound granularity (sub-tiles of a tile)
+constexpr int kPruneMaxR = 48;  // exact-tile shared memory bound ((32 + 2R)^2 samples, two buffers)
+
+template <typename T>
+__global__ void __launch_bounds__(256) k1p_tiles_kernel(
+    const T* __restrict__ f, int64_t H, int64_t W, int64_t ld, int64_t t_lo, int64_t t_hi,
+    int tiles_x, int stx, T* __restrict__ smax_all, T* __restrict__ smin_int,
+    unsigned long long* __restrict__ red, const PlanArgs pa) {
+  pdl_wait();  // statistics reset
+  pdl_trigger();
+  if (pa.fb_reset && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *pa.fb_reset = 0ull;
+  if (pa.zero_bytes) {  // fused pipeline: clear the K3 accumulator
+    const int64_t n16 = (int64_t)(pa.zero_bytes / 16);
+    const int64_t nth = (int64_t)gridDim.x * gridDim.y * blockDim.x;
+    uint4* z = static_cast<uint4*>(pa.zero);
+    for (int64_t i = ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+         i < n16; i += nth)
+      z[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  // warp w: tile (blockIdx.x * 8 + w, blockIdx.y); lane: a column, 32 rows;
+  // the 8x8 sub-tile maxima (every buffer row) and minima (rows in
+  // [t_lo, t_hi)) go to smax_all / smin_int
+  constexpr int SUB = kPruneSub, NSG = kPruneTile / kPruneSub;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tx = blockIdx.x * 8 + w, ty = blockIdx.y;
+  const int64_t x = (int64_t)tx * kPruneTile + lane;
+  const int64_t y0 = (int64_t)ty * kPruneTile;
+  T gmx[NSG], gmn[NSG];
+  T smx = neg_inf<T>(), wmn = T(INFINITY);
+  unsigned long long bad = 0;
+#pragma unroll
+  for (int g = 0; g < NSG; ++g) {
+    gmx[g] = neg_inf<T>();
+    gmn[g] = T(INFINITY);
+  }
+  if (tx < tiles_x && x < W) {
+    const int nr = (int)smin<int64_t>(kPruneTile, H - y0);
+    const T* col = f + y0 * ld + x;
+    T v[kPruneTile];
+#pragma unroll
+    for (int r = 0; r < kPruneTile; ++r) v[r] = r < nr ? __ldg(col + (int64_t)r * ld) : T(0);
+#pragma unroll
+    for (int r = 0; r < kPruneTile; ++r) {
+      if (r >= nr) break;
+      gmx[r / SUB] = vmax(gmx[r / SUB], v[r]);  // a window may reach into halo rows
+      const int64_t y = y0 + r;
+      if (y >= t_lo && y < t_hi) {  // T and the statistics: interior rows only
+        gmn[r / SUB] = fmin(gmn[r / SUB], v[r]);
+        smx = vmax(smx, v[r]);
+        bad += isfinite(v[r]) ? 0 : 1;  // image.py:16
+      }
+    }
+  }
+  // fold 8 columns (lanes) per sub-tile
+#pragma unroll
+  for (int g = 0; g < NSG; ++g) {
+    wmn = fmin(wmn, gmn[g]);
+    for (int o = 1; o < SUB; o <<= 1) {
+      gmx[g] = vmax(gmx[g], __shfl_xor_sync(0xffffffffu, gmx[g], o));
+      gmn[g] = fmin(gmn[g], __shfl_xor_sync(0xffffffffu, gmn[g], o));
+    }
+  }
+  if (tx < tiles_x && (lane & (SUB - 1)) == 0) {
+    const int sx = tx * NSG + lane / SUB;
+    if (sx < stx) {
+#pragma unroll
+      for (int g = 0; g < NSG; ++g) {
+        const int64_t sy = (int64_t)ty * NSG + g;
+        if (sy * SUB < H) {
+          smax_all[sy * stx + sx] = gmx[g];
+          smin_int[sy * stx + sx] = gmn[g];
+        }
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    wmn = fmin(wmn, __shfl_xor_sync(0xffffffffu, wmn, o));
+    smx = vmax(smx, __shfl_xor_sync(0xffffffffu, smx, o));
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  // one atomic per CTA for each statistic (per-warp atomics on the same
+  // three words serialised this pass)
+  __shared__ T s_mn[8], s_mx[8];
+  if (lane == 0) {
+    s_mn[w] = wmn;
+    s_mx[w] = smx;
+    if (bad) atomicAdd(&red[3], bad);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T a = s_mn[0], c = s_mx[0];
+    for (int k = 1; k < 8; ++k) {
+      a = fmin(a, s_mn[k]);
+      c = vmax(c, s_mx[k]);
+    }
+    if (a < T(INFINITY)) atomicMin(&red[1], ord_bits((double)a));
+    if (c > neg_inf<T>()) atomicMax(&red[2], ord_bits((double)c));
+  }
+}
+
+__global__ void k1p_init_kernel(double* stats, unsigned* done, unsigned long long* slots) {
+  pdl_wait();
+  pdl_trigger();
+  init_stats(stats, done);
+  slots[0] = ord_bits(-INFINITY);
+  slots[1] = slots[2] = 0ull;
+}
+
+// U_t for every tile with interior pixels (the max over its sub-tiles s of
+// (max of the sub-tile maxima within nbs = ceil(R/8) sub-tile steps) -
+// sub-tile minimum); Umax into slots[0].  Block = 256 / NS tiles of one tile row x
+// their NS sub-tiles each.
+template <typename T>
+__global__ void __launch_bounds__(256) k1p_bounds_kernel(
+    int tiles_x, int tiles_y, int stx, int sty, int nbs, const T* __restrict__ smax_all,
+    const T* __restrict__ smin_int, double* __restrict__ U, unsigned long long* __restrict__ slots) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int NSG = kPruneTile / kPruneSub, NS = NSG * NSG;  // sub-tiles per tile
+  const int k = threadIdx.x / NS, sub = threadIdx.x % NS;
+  const int tx = blockIdx.x * (256 / NS) + k, ty = blockIdx.y;
+  const int sx = tx * NSG + (sub & (NSG - 1)), sy = ty * NSG + sub / NSG;
+  double u = -INFINITY;
+  if (tx < tiles_x && sx < stx && sy < sty) {
+    const T mn = smin_int[(int64_t)sy * stx + sx];
+    if (mn < T(INFINITY)) {
+      T m = neg_inf<T>();
+      const int y_lo = max(0, sy - nbs), y_hi = min(sty - 1, sy + nbs);
+      const int x_lo = max(0, sx - nbs), x_hi = min(stx - 1, sx + nbs);
+      for (int yy = y_lo; yy <= y_hi; ++yy) {
+        const T* row = smax_all + (int64_t)yy * stx;
+        for (int xx = x_lo; xx <= x_hi; ++xx) m = vmax(m, row[xx]);
+      }
+      u = (double)m - (double)mn;
+    }
+  }
+  for (int o = NS / 2; o; o >>= 1) u = fmax(u, __shfl_xor_sync(0xffffffffu, u, o));
+  if (sub == 0 && tx < tiles_x) U[(int64_t)ty * tiles_x + tx] = u;
+  for (int o = 16; o; o >>= 1) u = fmax(u, __shfl_xor_sync(0xffffffffu, u, o));
+  if ((threadIdx.x & 31) == 0 && u > -INFINITY) atomicMax(&slots[0], ord_bits(u));
+}
+
+// Exact M - f on the tiles a round selects (persistent CTAs stride over the
+// tiles).  round 1: U_t == Umax; round 2: T < U_t < Umax, T = red[0] after
+// round 1.  The window maximum is separable: rows then columns, each by
+// power-of-two span maxima (doubling) in shared memory; samples outside the
+// buffer are -inf (the clamped window).
+template <typename T>
+__global__ void __launch_bounds__(256) k1p_exact_kernel(
+    const T* __restrict__ f, int64_t H, int64_t W, int64_t ld, int R, int64_t t_lo, int64_t t_hi,
+    int tiles_x, int ntiles, int round, const double* __restrict__ U,
+    const unsigned long long* __restrict__ slots, unsigned long long* __restrict__ red) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  pdl_wait();
+  pdl_trigger();
+  const int tid = threadIdx.x;
+  const int TS = kPruneTile, IW = TS + 2 * R, win = 2 * R + 1;
+  T* a = reinterpret_cast<T*>(smem_raw);  // [IW][IW] samples / row spans
+  T* b = a + IW * IW;                     // [IW][IW] ping-pong
+  __shared__ double dred[8];
+  const double umax = ord_value(slots[0]);
+  const double tcur = ord_value(red[0]);  // T after round 1 (round 2 only)
+  double tmax = 0.0;
+  __shared__ int s_list[256], s_n;
+  // the CTA's 256 threads test 256 tile bounds at once; the selected tiles
+  // are then evaluated one after another by the whole CTA
+  // (tile t goes to CTA t mod gridDim: selected tiles cluster in space, so
+  // neighbours land on different CTAs)
+  for (int base = 0; base * (int64_t)gridDim.x < ntiles; base += 256) {
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+    const int64_t t = (int64_t)(base + tid) * gridDim.x + blockIdx.x;
+    if (t < ntiles) {
+      const double u = U[t];
+      const bool sel = !(SBF_K1P_DBG & 1) && (round == 1 ? (u == umax && u > 0.0) : (u > tcur && u < umax));
+      if (sel) {
+        s_list[atomicAdd(&s_n, 1)] = (int)t;
+        atomicAdd(const_cast<unsigned long long*>(slots) + round, 1ull);  // tiles evaluated per round (diagnostic)
+      }
+    }
+    __syncthreads();
+    const int nsel = s_n;
+  for (int si = 0; si < nsel; ++si) {
+    const int t = s_list[si];
+    const int ty = t / tiles_x, tx = t - ty * tiles_x;
+    const int64_t y0 = (int64_t)ty * TS - R, x0 = (int64_t)tx * TS - R;
+    // warp w takes rows w, w + 8, ...; lane takes columns lane + 32 q
+    // (q < 4: IW <= 128); the loops are unrolled so that each thread's
+    // shared-memory reads of a pass are in flight together
+    const int lane = tid & 31, wp = tid >> 5;
+    constexpr int QC = (kPruneTile + 2 * kPruneMaxR + 31) / 32;  // column slots per lane
+    {
+      // every load of the region issued before any store (one latency)
+      constexpr int RR = (kPruneTile + 2 * kPruneMaxR + 7) / 8;  // rows per warp
+      T v[RR][QC];
+#pragma unroll
+      for (int i = 0; i < RR; ++i) {
+        const int r = wp + 8 * i;
+        const int64_t y = y0 + r;
+        const bool rok = r < IW && y >= 0 && y < H;
+#pragma unroll
+        for (int q = 0; q < QC; ++q) {
+          const int c = lane + 32 * q;
+          const int64_t x = x0 + c;
+          v[i][q] = (rok && c < IW && x >= 0 && x < W) ? __ldg(f + y * ld + x) : neg_inf<T>();
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < RR; ++i) {
+        const int r = wp + 8 * i;
+#pragma unroll
+        for (int q = 0; q < QC; ++q) {
+          const int c = lane + 32 * q;
+          if (r < IW && c < IW) a[r * IW + c] = v[i][q];
+        }
+      }
+    }
+    __syncthreads();
+    // the tile's own samples (for M - f) stay in registers
+    T fown[kPruneTile / 8];
+#pragma unroll
+    for (int i = 0; i < kPruneTile / 8; ++i) fown[i] = a[(R + wp + 8 * i) * IW + R + lane];
+    // row direction: a[r][c] = max over [c, c + span) by doubling
+    T* src = a;
+    T* dst = b;
+    int span = 1;
+    while (2 * span <= win) {
+#pragma unroll 2
+      for (int r = wp; r < IW; r += 8) {
+        T* d = dst + r * IW;
+        const T* sr = src + r * IW;
+#pragma unroll
+        for (int q = 0; q < QC; ++q) {
+          const int c = lane + 32 * q;
+          if (c < IW) d[c] = c + span < IW ? vmax(sr[c], sr[c + span]) : sr[c];
+        }
+      }
+      __syncthreads();
+      T* tt = src;
+      src = dst;
+      dst = tt;
+      span *= 2;
+    }
+    // row maxima of the tile's output columns: rm[r][j] = max over [j, j + win)
+#pragma unroll 4
+    for (int r = wp; r < IW; r += 8) dst[r * IW + lane] = vmax(src[r * IW + lane], src[r * IW + lane + win - span]);
+    __syncthreads();
+    // column direction on rm (IW rows x TS columns, in dst)
+    src = dst;
+    dst = (src == a) ? b : a;
+    span = 1;
+    while (2 * span <= win) {
+#pragma unroll 4
+      for (int r = wp; r < IW; r += 8)
+        dst[r * IW + lane] = r + span < IW ? vmax(src[r * IW + lane], src[(r + span) * IW + lane]) : src[r * IW + lane];
+      __syncthreads();
+      T* tt = src;
+      src = dst;
+      dst = tt;
+      span *= 2;
+    }
+#pragma unroll
+    for (int k = 0; k < kPruneTile / 8; ++k) {
+      const int i = wp + 8 * k;
+      const int64_t y = (int64_t)ty * TS + i, x = (int64_t)tx * TS + lane;
+      if (y < t_lo || y >= t_hi || y >= H || x >= W) continue;
+      const T m = vmax(src[i * IW + lane], src[(i + win - span) * IW + lane]);
+      tmax = fmax(tmax, (double)m - (double)fown[k]);  // maxfilter.py:61
+    }
+    __syncthreads();  // a / b are reloaded for the next tile
+  }
+    __syncthreads();  // s_list / s_n are rewritten for the next group
+  }
+  for (int o = 16; o; o >>= 1) tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+  if ((tid & 31) == 0) dred[tid >> 5] = tmax;
+  __syncthreads();
+  if (tid == 0) {
+    for (int wv = 1; wv < 8; ++wv) tmax = fmax(tmax, dred[wv]);
+    atomicMax(&red[0], ord_bits(tmax));
+  }
+}
+
+// statistics finalisation and (fused pipeline) the plan, after round 2: a
+// one-warp kernel, so the exact-tile kernel stays small (its code is fetched
+// cold by the few CTAs that evaluate a tile)
+__global__ void k1p_final_kernel(unsigned long long* __restrict__ red, const PlanArgs pa) {
+  __shared__ sbf_plan s_plan;
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0) finalize_stats(reinterpret_cast<double*>(red) - 4);
+  __syncwarp();
+  if (pa.on)
+    plan_warp(threadIdx.x == 0 ? (reinterpret_cast<double*>(red) - 4)[0] : 0.0, pa.sigma_r, pa.eps,
+              pa.rule, pa.log_2_over_eps, pa.plan, pa.terms, pa.cap, 0, 0, s_plan);
+}
+
 // R == 0: T = 0 by definition (maxfilter.py:58-59); statistics only.
 template <typename T>
 __global__ void stats_only_kernel(const T* __restrict__ f, int64_t W, int64_t ld, int64_t t_lo,
@@ -736,6 +1058,52 @@ int run(const void* fv, int64_t H, int64_t W, int64_t ld, int R, int64_t t_lo, i
     stats_only_kernel<T><<<2 * 148, 256, 0, st>>>(f, W, ld, t_lo, t_hi, static_cast<T*>(M_out), H,
                                                   red);
     SBF_CHECK_LAUNCH();
+  } else if (SBF_K1_PRUNE && !M_out && H * W >= ((int64_t)4 << 20) &&
+             R <= (sizeof(T) == 4 ? kPruneMaxR : 24)) {
+    // pruned exact T (no M image): tile bounds, then exact tiles only where
+    // a tile could raise T
+    const int tiles_x = (int)((W + kPruneTile - 1) / kPruneTile);
+    const int tiles_y = (int)((H + kPruneTile - 1) / kPruneTile);
+    const int ntiles = tiles_x * tiles_y;
+    const int stx = (int)((W + kPruneSub - 1) / kPruneSub), sty = (int)((H + kPruneSub - 1) / kPruneSub);
+    const size_t nsub = (size_t)stx * sty;
+    char* w = static_cast<char*>(ws);
+    T* smax_all = reinterpret_cast<T*>(w);
+    T* smin_int = smax_all + nsub;
+    double* U = reinterpret_cast<double*>(w + align_up(2 * nsub * sizeof(T)));
+    unsigned long long* slots =
+        reinterpret_cast<unsigned long long*>(w + align_up(2 * nsub * sizeof(T)) + align_up((size_t)ntiles * 8));
+    SBF_REQUIRE(align_up(2 * nsub * sizeof(T)) + align_up((size_t)ntiles * 8) + 64 <=
+                    align_up((size_t)(H * W) * sizeof(T)),
+                SBF_ERR_WORKSPACE, "local_range workspace too small");
+    SBF_CHECK_CUDA(launch_pdl(k1p_init_kernel, dim3(1), dim3(1), 0, st, stats, done, slots));
+    SBF_CHECK_LAUNCH();
+    SBF_CHECK_CUDA(launch_pdl(k1p_tiles_kernel<T>, dim3((unsigned)((tiles_x + 7) / 8), (unsigned)tiles_y),
+                              dim3(256), 0, st, f, H, W, ld, t_lo, t_hi, tiles_x, stx, smax_all, smin_int,
+                              red, pa));
+    SBF_CHECK_LAUNCH();
+    const int nbs = (R + kPruneSub - 1) / kPruneSub;
+    constexpr int kTilesPerBoundsBlock = 256 / ((kPruneTile / kPruneSub) * (kPruneTile / kPruneSub));
+    SBF_CHECK_CUDA(launch_pdl(k1p_bounds_kernel<T>,
+                              dim3((unsigned)((tiles_x + kTilesPerBoundsBlock - 1) / kTilesPerBoundsBlock),
+                                   (unsigned)tiles_y),
+                              dim3(256), 0, st, tiles_x, tiles_y, stx, sty, nbs,
+                              static_cast<const T*>(smax_all), static_cast<const T*>(smin_int), U, slots));
+    SBF_CHECK_LAUNCH();
+    const int IW = kPruneTile + 2 * R;
+    const size_t smem = (size_t)2 * IW * IW * sizeof(T);
+    SBF_CHECK_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(k1p_exact_kernel<T>), smem));
+    const int per_sm = (int)smax<int64_t>(1, smin<int64_t>(4, (int64_t)(227 * 1024) / (int64_t)(smem + 1024)));
+    const int grid = (int)smin<int64_t>(ntiles, (int64_t)device_sm_count() * per_sm);
+    for (int round = 1; round <= ((SBF_K1P_DBG & 2) ? 0 : 2); ++round) {
+      SBF_CHECK_CUDA(launch_pdl(k1p_exact_kernel<T>, dim3((unsigned)grid), dim3(256), smem, st, f, H, W, ld,
+                                R, t_lo, t_hi, tiles_x, ntiles, round, static_cast<const double*>(U),
+                                static_cast<const unsigned long long*>(slots), red));
+      SBF_CHECK_LAUNCH();
+    }
+    SBF_CHECK_CUDA(launch_pdl(k1p_final_kernel, dim3(1), dim3(32), 0, st, red, pa));
+    SBF_CHECK_LAUNCH();
+    return SBF_OK;  // k1p_final_kernel wrote the final statistics (and the plan)
   } else if (SBF_K1_STREAM && sizeof(T) == 4 && R <= 24 && H * W >= (int64_t)4 << 20 &&
              stream_smem_bytes<T>(R) <= 200 * 1024) {
     // measured on B200 (K1 alone, us): config 4 (4096^2, R=18) 189 -> 157;

@@ -429,3 +429,44 @@ def test_strips_with_streamed_epilogue(mode):
         lib.sbf_set_fused_epilogue(prev)
     assert float(Tg[0]) == full.plan.T
     assert_close_image(gather_strips(outs, strips), full.image, 2e-3, 2e-4)
+
+
+@pytest.mark.parametrize("shape,dtype,R,kind,rows", [
+    ((2048, 2048), "float32", 18, "noise", None),
+    ((2048, 2048), "float32", 40, "rects", None),
+    ((2048, 2048), "float32", 3, "rects", (100, 1900)),
+    ((1024, 4096), "float64", 20, "rects", None),
+    ((2048, 2176), "float32", 36, "ramp", (36, 2012)),
+    ((2048, 2048), "float32", 9, "const", None),
+])
+def test_pruned_local_range_T_exact(shape, dtype, R, kind, rows):
+    """Images of >= 4 Mpx without an M image take the pruned K1 (tile bounds,
+    exact evaluation of the tiles that can raise T): T, min, max must equal
+    the full evaluation bit for bit, including row-restricted (strip) T,
+    uniform noise (loose bounds, many tiles evaluated) and a constant image."""
+    from oracle import coracle as CO
+    from paper_1203_5128_b200.image import stage
+    from paper_1203_5128_b200.maxfilter import local_range
+    rng = np.random.default_rng(R)
+    H, W = shape
+    if kind == "noise":
+        img = rng.uniform(0, 255, shape)
+    elif kind == "const":
+        img = np.full(shape, 77.0)
+    elif kind == "ramp":
+        img = np.add.outer(np.arange(H) * 0.01, np.arange(W) * 0.02) + rng.normal(0, 0.5, shape)
+    else:
+        img = np.zeros(shape)
+        for _ in range(40):
+            h, w = rng.integers(H // 16, H // 4), rng.integers(W // 16, W // 4)
+            y, x = rng.integers(0, H - h), rng.integers(0, W - w)
+            img[y:y + h, x:x + w] = rng.uniform(0, 255)
+        img = np.clip(img + rng.normal(0, 8, shape), 0, 255)
+    img = img.astype(dtype)
+    lo, hi = rows if rows is not None else (0, H)
+    stats, _ = local_range(stage(img), R, t_rows=(lo, hi))
+    st = stats.cpu().numpy()
+    M = CO.max_filter_2d(img.astype(np.float64), R)
+    D = M[lo:hi] - img[lo:hi].astype(np.float64)
+    assert st[0] == float(D.max())
+    assert st[1] == float(img[lo:hi].min()) and st[2] == float(img[lo:hi].max())

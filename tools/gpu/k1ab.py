@@ -35,5 +35,7 @@ for path in libs:
         for _ in range(n): run()
         e1.record(); e1.synchronize()
         us = e0.elapsed_time(e1) / n * 1e3
+        T2 = float(stats[0].item())
+        st2 = stats[1:3].tolist()
         gbs = H * W * f.element_size() / (us * 1e-6) / 1e9
-        print(f"{os.path.basename(path):20s} cfg{cfg} {H}x{W} R={R} K1 {us:8.1f} us  ({gbs:6.0f} GB/s of f)  T={T!r} sumM={msum!r}", flush=True)
+        print(f"{os.path.basename(path):20s} cfg{cfg} {H}x{W} R={R} K1 {us:8.1f} us  ({gbs:6.0f} GB/s of f)  T={T!r} T(no M)={T2!r} min/max={st2} sumM={msum!r}", flush=True)

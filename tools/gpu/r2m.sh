@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/r2m_tests.log 2>&1; echo "tests rc=$?"; tail -n 2 gpurun_out/r2m_tests.log; grep -E "^FAILED" gpurun_out/r2m_tests.log | head
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/r2m_bench4.log 2>&1; echo "bench4 rc=$?"; tail -n 1 gpurun_out/r2m_bench4.log | cut -c 1-200
+timeout 600 python bench.py --config 2 --no-cpu-baseline > gpurun_out/r2m_bench2.log 2>&1; echo "bench2 rc=$?"; tail -n 1 gpurun_out/r2m_bench2.log | cut -c 1-200

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/r2p_tests.log 2>&1; echo "tests rc=$?"; tail -n 2 gpurun_out/r2p_tests.log; grep -E "^FAILED" gpurun_out/r2p_tests.log | head
+timeout 900 python bench.py > gpurun_out/r2p_bench4.log 2>&1; echo "bench4 rc=$?"; tail -n 1 gpurun_out/r2p_bench4.log | cut -c 1-200
+timeout 900 python bench.py --config 5 --steps 3 > gpurun_out/r2p_bench5.log 2>&1; echo "bench5 rc=$?"; tail -n 1 gpurun_out/r2p_bench5.log | cut -c 1-200
