@@ -666,10 +666,9 @@ static int launch_sweep_path(const FilterLaunch& a, const SweepEntry& w, int r, 
   int rc = w.launch(map, p, a.stream);
   if (rc != SBF_OK) return rc;
   if (!p.fused_epi) {
-    const int64_t n = rows_out * a.W;
-    const unsigned grid = (unsigned)smin<int64_t>((n + 255) / 256, (int64_t)device_sm_count() * 8);
+    const unsigned grid = (unsigned)smin<int64_t>(rows_out, (int64_t)device_sm_count() * 8);
     SBF_CHECK_CUDA(launch_pdl(sweep_divide_kernel, dim3(grid), dim3(256), 0, a.stream,
-                              static_cast<const unsigned long long*>(p.acc), n, a.W, a.out_lo, a.f,
+                              static_cast<const unsigned long long*>(p.acc), rows_out, a.W, a.out_lo, a.f,
                               a.ld, a.dtype, a.out, a.out_dtype, a.plan, a.stats, a.fallback));
     SBF_CHECK_LAUNCH();
   }

@@ -776,7 +776,7 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
 // the sweep's last items (which serialised the tail: 0.23 ms of a 2.0 ms
 // config-4 sweep).  Same decode and arithmetic as the fused epilogue.
 static __global__ void __launch_bounds__(256) sweep_divide_kernel(
-    const unsigned long long* __restrict__ acc, int64_t n, int64_t W, int64_t out_lo,
+    const unsigned long long* __restrict__ acc, int64_t rows, int64_t W, int64_t out_lo,
     const void* __restrict__ fo, int64_t fo_ld, int fo_dtype, void* __restrict__ out, int out_dtype,
     const sbf_plan* __restrict__ plan, const double* __restrict__ stats,
     unsigned long long* __restrict__ fallback) {
@@ -788,32 +788,35 @@ static __global__ void __launch_bounds__(256) sweep_divide_kernel(
   const int nexp = ilogb(fmax(maxdev, 1.0)) + 1;
   const double inv_nscale = ldexp(1.0, nexp - 29), inv_dscale = ldexp(1.0, -29);
   unsigned long long bad = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const long long sum = (long long)__ldcs(acc + i);
-    const int lo = (int)(unsigned)(sum & 0xffffffffll);
-    const long long hi = (sum - (long long)lo) >> 32;
-    const double num = (double)hi * inv_nscale, den = (double)lo * inv_dscale;
-    const bool is_bad = !(den > 0.0);  // bilateral.py:244
-    bad += is_bad ? 1 : 0;
-    const int64_t y = i / W, x = i - y * W;
-    const int64_t fi = (out_lo + y) * fo_ld + x;
-    if (out_dtype == SBF_F32) {
-      float o;
-      if (is_bad)
-        o = fo_dtype == SBF_F32 ? static_cast<const float*>(fo)[fi]
-                                : (float)static_cast<const double*>(fo)[fi];
-      else
-        o = (float)(num / den) + centerf;
-      static_cast<float*>(out)[i] = o;
-    } else {
-      double o;
-      if (is_bad)
-        o = fo_dtype == SBF_F32 ? (double)static_cast<const float*>(fo)[fi]
-                                : static_cast<const double*>(fo)[fi];
-      else
-        o = num / den + centerd;
-      static_cast<double*>(out)[i] = o;
+  // rows over the grid, columns over the threads (no 64-bit index division)
+  for (int64_t y = blockIdx.x; y < rows; y += gridDim.x) {
+    const unsigned long long* arow = acc + y * W;
+    const int64_t frow = (out_lo + y) * fo_ld;
+    for (int64_t x = threadIdx.x; x < W; x += blockDim.x) {
+      const long long sum = (long long)__ldcs(arow + x);
+      const int lo = (int)(unsigned)(sum & 0xffffffffll);
+      const long long hi = (sum - (long long)lo) >> 32;
+      const double num = (double)hi * inv_nscale, den = (double)lo * inv_dscale;
+      const bool is_bad = !(den > 0.0);  // bilateral.py:244
+      bad += is_bad ? 1 : 0;
+      const int64_t i = y * W + x;
+      if (out_dtype == SBF_F32) {
+        float o;
+        if (is_bad)
+          o = fo_dtype == SBF_F32 ? static_cast<const float*>(fo)[frow + x]
+                                  : (float)static_cast<const double*>(fo)[frow + x];
+        else
+          o = (float)(num / den) + centerf;
+        static_cast<float*>(out)[i] = o;
+      } else {
+        double o;
+        if (is_bad)
+          o = fo_dtype == SBF_F32 ? (double)static_cast<const float*>(fo)[frow + x]
+                                  : static_cast<const double*>(fo)[frow + x];
+        else
+          o = num / den + centerd;
+        static_cast<double*>(out)[i] = o;
+      }
     }
   }
   for (int o = 16; o; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
