@@ -48,7 +48,9 @@ UNIT = "Mpixel/s"
 OPS_PER_PX_TERM = 132   # phasor 4 + f*c,f*s 2 + 4 images x 6 line passes x 5 + acc 6
 OPS_PER_PX = 10         # local range ~8 + divide ~2
 L2_FLUSH_BYTES = 256 << 20
-E2E_LANES = 4  # streams of the batch API in the e2e leg (copy engine both ways)
+E2E_LANES = 3  # streams of the batch API in the e2e leg (copy engine both ways); measured
+# on B200 (64 config-4 images): 2 lanes 147 ms/step, 3 lanes 125 ms (steady), 4 lanes
+# 125-298 ms (outliers)
 PEAK_FP32_NOMINAL = 148 * 128 * 1.965e9 / 1e12  # T lane-ops/s (FADD/FMUL/FFMA = 1 op)
 DFMA_PEAK_MEASURED = 16.99  # T DFMA/s on the pool's B200 (profiles/r2_fma_probe.txt)
 DATA = "synthetic (SURVEY.md Appendix A seeded generator; BASELINE names no dataset)"
@@ -524,7 +526,7 @@ def run_ours(args, rank, world, dev):
         launches=KERNELS_PER_IMAGE * len(imgs) * args.steps,
         e2e=dict(value=e2e_value, unit=UNIT, h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h),
                  ms_per_step=e2e_ms / args.steps,
-                 path=("shiftable_bf_batch (4 streams): pinned host images -> copy-engine H2D, "
+                 path=(f"shiftable_bf_batch ({E2E_LANES} streams): pinned host images -> copy-engine H2D, "
                        "kernels, copy-engine D2H of each result into pinned host memory; "
                        "both PCIe directions overlap other images' kernels") if cfg == 4 else
                       ("shiftable_bf on a pinned host tensor: SM-staged H2D, K1..K3, the K3 "

@@ -93,8 +93,13 @@ struct PlanArgs {
 // predecessor reads or writes, which returns once the predecessor grid has
 // completed and flushed (a no-op for an ordinary launch).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#ifndef SBF_PDL_EARLY
+#define SBF_PDL_EARLY 1  // 0: dependents are scheduled only when the whole primary grid exits
+#endif
 __device__ __forceinline__ void pdl_trigger() {
+#if SBF_PDL_EARLY
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 }
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
