@@ -550,6 +550,9 @@ static int launch_split_path(const FilterLaunch& a, const SplitEntry& se, int r,
 }
 
 // ---- K3 sweep path ----
+#ifndef SBF_SWEEP_MAX_BAND
+#define SBF_SWEEP_MAX_BAND 768  // rows per sweep item at most (measured config 4: 512 1.910 ms, 768 1.879, 1024 1.883)
+#endif
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -624,7 +627,7 @@ static int launch_sweep_path(const FilterLaunch& a, const SweepEntry& w, int r, 
   p.img_H = a.img_H;
   p.out_lo = (int)a.out_lo;
   p.out_hi = (int)a.out_hi;
-  p.band = (int)smin<int64_t>(rows_out, 512);
+  p.band = (int)smin<int64_t>(rows_out, SBF_SWEEP_MAX_BAND);
   p.nstrips = (int)sweep_strips(w, a.W);
   p.r = r;
   p.alpha = (float)alpha;
