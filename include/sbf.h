@@ -321,6 +321,16 @@ int sbf_set_k3_events(void* before, void* after);
  * every term has landed on it): 1 (default) = when out is host memory,
  * 2 = always, 0 = never.  Returns the previous setting (-1: bad mode). */
 int sbf_set_fused_epilogue(int mode);
+/* K3 sweep (r <= 5), this thread: which kernel serves device outputs --
+ * 0 (default) = the phase-separated sweep (two 128-thread CTAs per SM,
+ * 128-column strips), 1 = the warp-specialised sweep (one 512-thread CTA per
+ * SM, 252-column strips, V / H warpgroups over mbarriers) for images of at
+ * least 2^20 pixels, 2 = the warp-specialised sweep for every device output.
+ * Same results within fp32 rounding of the strip geometry; measured slower
+ * on B200, kept as a tested alternative.  Page-locked host
+ * outputs always take the phase-separated sweep with its fused epilogue.
+ * Returns the previous setting. */
+int sbf_set_sweep_variant(int mode);
 int sbf_fp32_probe(int blocks, int threads, int iters, float* out_dev, void* stream);
 
 #ifdef __cplusplus

@@ -83,6 +83,7 @@ _SIGS = {
     "sbf_set_stage_mask": (_int, [_int]),
     "sbf_set_k3_events": (_int, [_vp, _vp]),
     "sbf_set_fused_epilogue": (_int, [_int]),
+    "sbf_set_sweep_variant": (_int, [_int]),
     "sbf_pgm_decode": (_int, [_vp, _int, _i64, _vp, _vp]),
     "sbf_pgm_encode": (_int, [_vp, _int, _i64, _int, _vp, _vp]),
     "sbf_direct_bf": (_int, [_vp, _int, _i64, _i64, _i64, _int, _vp, _dbl, _int, _vp, _int, _vp]),

@@ -68,6 +68,13 @@ static const SplitEntry* find_split(const sbf_spatial& sp, int precision) {
 #define SBF_SWEEP_ON 1
 #endif
 static thread_local int g_sweep_on = SBF_SWEEP_ON;
+// warp-specialised sweep (sbf_sweepw.cuh), device outputs only: 0 never
+// (default: measured slower than the phase-separated sweep),
+// 1 images of at least SBF_SWEEPW_MIN_PX pixels, 2 every device output
+#ifndef SBF_SWEEPW_MIN_PX
+#define SBF_SWEEPW_MIN_PX (1 << 20)
+#endif
+static thread_local int g_sweep_w = 0;
 
 static const SweepEntry* find_sweep(const sbf_spatial& sp, int precision) {
   static const std::vector<SweepEntry> reg = {
@@ -639,18 +646,6 @@ static int launch_sweep_path(const FilterLaunch& a, const SweepEntry& w, int r, 
   p.stats = a.stats;
   p.fallback = a.fallback;
   p.hdr_guard = g_hdr_guard;
-  // TMA view of the fp32 image: 128 columns x `rows` rows per box,
-  // zero-filled outside the buffer
-  CUtensorMap map;
-  cuuint64_t dims[2] = {(cuuint64_t)a.W, (cuuint64_t)a.H};
-  cuuint64_t strides[1] = {(cuuint64_t)p.ld * 4};
-  cuuint32_t box[2] = {132u, (cuuint32_t)w.rows};  // SweepCfg::FCOLS
-  cuuint32_t es[2] = {1u, 1u};
-  const CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(p.f), dims,
-                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  SBF_REQUIRE(cr == CUDA_SUCCESS, SBF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
   // the divide/fallback epilogue: fused into the sweep (segment by segment,
   // as items complete) when the output is page-locked host memory, so its
   // PCIe writes overlap the sweep; a full-width kernel after the sweep for
@@ -664,9 +659,38 @@ static int launch_sweep_path(const FilterLaunch& a, const SweepEntry& w, int r, 
       cudaGetLastError();
   }
   p.fused_epi = (g_fused_epi == 2 || out_host) ? 1 : 0;
+  // device outputs of large images: the warp-specialised sweep (wider strips)
+  const bool use_w = !p.fused_epi && w.launch_w &&
+                     (g_sweep_w == 2 || (g_sweep_w == 1 && rows_out * a.W >= SBF_SWEEPW_MIN_PX));
+  if (use_w) p.nstrips = (int)((a.W + w.wc_w - 1) / w.wc_w);
+  // TMA view of the fp32 image: one box of f per chunk of stream steps,
+  // zero-filled outside the buffer
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)a.W, (cuuint64_t)a.H};
+  cuuint64_t strides[1] = {(cuuint64_t)p.ld * 4};
+  cuuint32_t box[2] = {132u, (cuuint32_t)w.rows};  // SweepCfg::FCOLS
+  if (use_w) {
+    box[0] = (cuuint32_t)w.fcols_w;
+    box[1] = (cuuint32_t)w.rows_w;
+  }
+  cuuint32_t es[2] = {1u, 1u};
+  const CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(p.f), dims,
+                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SBF_REQUIRE(cr == CUDA_SUCCESS, SBF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  CUtensorMap amap = map;  // the output pixels' own f, one box per chunk (warp-specialised sweep)
+  if (use_w) {
+    cuuint32_t abox[2] = {(cuuint32_t)w.afc_w, (cuuint32_t)w.afr_w};
+    const CUresult ar = enc(&amap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(p.f), dims,
+                            strides, abox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    SBF_REQUIRE(ar == CUDA_SUCCESS, SBF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)ar);
+  }
   if (!(g_stage_mask & 1)) return SBF_OK;
   if (g_k3_ev[0]) SBF_CHECK_CUDA(cudaEventRecord(g_k3_ev[0], a.stream));
-  int rc = w.launch(map, p, a.stream);
+  int rc = use_w ? w.launch_w(map, amap, p, a.stream) : w.launch(map, p, a.stream);
   if (rc != SBF_OK) return rc;
   if (!p.fused_epi) {
     const unsigned grid = (unsigned)smin<int64_t>(rows_out, (int64_t)device_sm_count() * 8);
@@ -880,6 +904,12 @@ int sbf_set_fused_epilogue(int on) {
   const int prev = sbf::g_fused_epi;
   if (on < 0 || on > 2) return -1;
   sbf::g_fused_epi = on;
+  return prev;
+}
+
+int sbf_set_sweep_variant(int mode) {
+  const int prev = sbf::g_sweep_w;
+  if (mode >= 0 && mode <= 2) sbf::g_sweep_w = mode;
   return prev;
 }
 

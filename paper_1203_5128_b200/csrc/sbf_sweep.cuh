@@ -858,10 +858,16 @@ struct SweepEntry {
   size_t (*smem)(int);
   void (*geom)(int*, int*, int*, int*);
   int rows;  // stream steps per chunk (TMA box height)
+  // warp-specialised variant (sbf_sweepw.cuh; sbf_set_sweep_variant): device outputs only
+  int (*launch_w)(const CUtensorMap&, const CUtensorMap&, const SweepParams&, cudaStream_t);
+  size_t (*smem_w)(int);
+  int wc_w, rows_w, fcols_w, afc_w, afr_w;
 };
 
 #define SBF_SWEEP_ENTRY(R, P)                                                                \
   SweepEntry { R, P, &launch_sweep<R, P>, &sweep_smem_bytes<R, P>, &sweep_geometry<R, P>,   \
-               SweepCfg<R, P>::ROWS }
+               SweepCfg<R, P>::ROWS, &launch_sweepw<R, P>, &sweepw_smem_bytes<R, P>,        \
+               SweepWCfg<R, P>::WC, SweepWCfg<R, P>::L, SweepWCfg<R, P>::FCOLS,             \
+               SweepWCfg<R, P>::AFC, SweepWCfg<R, P>::GR }
 
 }  // namespace sbf

@@ -1,5 +1,5 @@
 // One K3 sweep instantiation per object (built with -DSBF_R=<r> -DSBF_P=<passes>).
-#include "sbf_sweep.cuh"
+#include "sbf_sweepw.cuh"
 
 namespace sbf {
 #define SBF_SCAT2(a, b, c) a##b##_##c

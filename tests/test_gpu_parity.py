@@ -407,6 +407,64 @@ def test_split_sweep_matches_strip_kernel_and_oracle(shape, sigma_s, sigma_r):
     assert float(np.abs(outs[0] - outs[1]).max()) < 5e-3
 
 
+@pytest.mark.parametrize("shape,sigma_s,sigma_r,dtype", [
+    ((300, 517), 2.0, 25.0, "float32"), ((777, 1031), 4.0, 30.0, "float32"),
+    ((130, 260), 1.0, 25.0, "float64"), ((64, 3000), 6.0, 20.0, "float32"),
+    ((40, 215), 6.0, 20.0, "float32"), ((513, 217), 3.0, 30.0, "float32")])
+def test_warp_specialised_sweep_vs_oracle(shape, sigma_s, sigma_r, dtype):
+    """The warp-specialised K3 sweep (sbf_set_sweep_variant(2): 252-column
+    strips, V / H warpgroups over mbarriers, two TMA views) against the oracle
+    and against the phase-separated sweep, on CUDA tensors (device outputs);
+    shapes cover one and several strips, partial last strips, bands shorter
+    than the halo warm-up and both input dtypes."""
+    import torch
+    lib = _lib.load()
+    rng = np.random.default_rng(shape[0] * 131 + shape[1])
+    img = (rng.random(shape) * 255).astype(dtype)
+    img[shape[0] // 3:, shape[1] // 2:] += 40.0
+    img = np.clip(img, 0, 255)
+    params = P.FilterParams(sigma_s=sigma_s, sigma_r=sigma_r, epsilon=0.01, precision="fp32")
+    ref = O.shiftable_bf(img.astype(np.float64), sigma_s, sigma_r, 0.01)
+    t = torch.from_numpy(img).cuda()
+    outs = {}
+    prev = lib.sbf_set_sweep_variant(0)
+    try:
+        for var in (0, 2):
+            lib.sbf_set_sweep_variant(var)
+            res = P.shiftable_bf(t, params)
+            assert (res.plan.T, res.plan.N, res.plan.M) == (ref["T"], ref["N"], ref["M"])
+            outs[var] = res.image.double().cpu().numpy()
+            assert_close_image(outs[var], ref["image"])
+        # repeated calls are bit-identical (fixed-point accumulation)
+        again = P.shiftable_bf(t, params).image.double().cpu().numpy()
+        assert np.array_equal(again, outs[2])
+    finally:
+        lib.sbf_set_sweep_variant(prev)
+    assert float(np.abs(outs[0] - outs[2]).max()) < 5e-3
+
+
+def test_warp_specialised_sweep_strips():
+    """Row strips (out_lo > 0, buffer row offsets, global row indices) through
+    the warp-specialised sweep equal the full-image filter."""
+    import torch
+    from paper_1203_5128_b200.dist import StripFilter, gather_strips, strip_halo, strip_plan
+    lib = _lib.load()
+    img = config_image(4, size=640)
+    params = P.FilterParams(sigma_s=6.0, sigma_r=20.0, epsilon=0.01, precision="fp32")
+    full = P.shiftable_bf(img, params)
+    t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+    strips = strip_plan(img.shape[0], 3, strip_halo(params))
+    prev = lib.sbf_set_sweep_variant(2)
+    try:
+        fs = [StripFilter([t[s.buf_lo:s.buf_hi]], s, img.shape[0], params) for s in strips]
+        Tg = torch.stack([f.local_T().clone() for f in fs]).max(dim=0).values
+        outs = [f.finish(Tg)[0].cpu().numpy() for f in fs]
+    finally:
+        lib.sbf_set_sweep_variant(prev)
+    assert float(Tg[0]) == full.plan.T
+    assert_close_image(gather_strips(outs, strips), full.image, 2e-3, 2e-4)
+
+
 @pytest.mark.parametrize("mode", [0, 2])
 def test_strips_with_streamed_epilogue(mode):
     """Strips (out_lo > 0, buffer row offsets) through K3 with the epilogue
