@@ -303,8 +303,9 @@ int sbf_stage_h2d(const void* host_src, int src_kind, int64_t n, void* dev_dst, 
  * window when M = 0 and it is cheaper), 2 = dual whenever M = 0. */
 int sbf_set_fp64_method(int mode);
 /* fp32 term sweeps, this thread: radii >= r (with an instantiation) run the
- * split column/row sweep instead of the fused strip kernel K3 (default 9;
- * 0 = always K3). */
+ * split column/row sweep instead of the fused strip kernels (default 6: the
+ * K3 sweep serves r <= 5; 0 = never the split sweep; -1 = restore the
+ * default). */
 int sbf_set_split_min_radius(int r);
 int sbf_num_specialisations(void);
 int sbf_specialisation(int i, int* r, int* passes, int* mode);

@@ -43,7 +43,11 @@ int launch_generic_terms(const FilterLaunch& a, double* nd);
 
 // radii at or above this use the split sweep when an instantiation exists
 // (fp32 precision); 0 disables the split path
-static thread_local int g_split_min_r = 9;  // measured crossover vs K3 on B200 (r=5..8: K3 faster)
+// (r <= 5: the K3 sweep; r = 6..8 measured on a 4096^2 image, K = 22: split
+// 3.12 / 3.19 ms vs the round-1 term kernel 3.16 / 3.38 ms, and the split sweep
+// is bit-reproducible)
+#define SBF_SPLIT_MIN_R_DEFAULT 6
+static thread_local int g_split_min_r = SBF_SPLIT_MIN_R_DEFAULT;
 
 static const SplitEntry* find_split(const sbf_spatial& sp, int precision) {
   static const std::vector<SplitEntry> reg = {
@@ -926,8 +930,8 @@ int sbf_set_stage_mask(int mask) {
 }
 
 int sbf_set_split_min_radius(int r) {
-  if (r < 0) return SBF_ERR_INVALID;
-  sbf::g_split_min_r = r;
+  if (r < -1) return SBF_ERR_INVALID;
+  sbf::g_split_min_r = r == -1 ? SBF_SPLIT_MIN_R_DEFAULT : r;
   return SBF_OK;
 }
 

@@ -403,7 +403,7 @@ def test_split_sweep_matches_strip_kernel_and_oracle(shape, sigma_s, sigma_r):
             assert_close_image(res.image, ref["image"])
             outs.append(res.image)
     finally:
-        lib.sbf_set_split_min_radius(9)
+        lib.sbf_set_split_min_radius(-1)
     assert float(np.abs(outs[0] - outs[1]).max()) < 5e-3
 
 
