@@ -270,6 +270,9 @@ __device__ __forceinline__ bool sweep_needs_hdr(const double* stats) {
 #ifndef SBF_SWEEP_STS4
 #define SBF_SWEEP_STS4 0  // V phase: one 16-byte shared store per step instead of two 8-byte ones
 #endif
+#ifndef SBF_SWEEP_ITEMS_PER_CTA
+#define SBF_SWEEP_ITEMS_PER_CTA 2  // band height: at least this many items per CTA
+#endif
 #ifndef SBF_SWEEP_ABL
 #define SBF_SWEEP_ABL 0  // phase ablation for timing studies (wrong results when != 0)
 #endif
@@ -359,7 +362,7 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
   int bandh = p.band;
   {
     const int per_band = max(1, p.nstrips * K_eval);
-    const int nb_min = (2 * (int)gridDim.x + per_band - 1) / per_band;
+    const int nb_min = (SBF_SWEEP_ITEMS_PER_CTA * (int)gridDim.x + per_band - 1) / per_band;
     const int b = (rows_all + nb_min - 1) / nb_min;
     bandh = max(min(b, p.band), min(4 * HALO, p.band));
   }

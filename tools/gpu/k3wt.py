@@ -5,7 +5,7 @@ sys.path.insert(0, os.getcwd())
 from paper_1203_5128_b200.workloads import config_image, CONFIGS
 libs = sys.argv[1:] or ["paper_1203_5128_b200/libsbf.so"]
 var = int(os.environ.get("SBF_VARIANT", "2"))
-imgs = {c: torch.from_numpy(np.ascontiguousarray(config_image(c), dtype=np.float32)).cuda() for c in (4, 2)}
+imgs = {c: torch.from_numpy(np.ascontiguousarray(config_image(c), dtype=np.float32)).cuda() for c in (4, 2, 1)}
 for path in libs:
     os.environ["SBF_LIB"] = path
     import paper_1203_5128_b200._lib as L
