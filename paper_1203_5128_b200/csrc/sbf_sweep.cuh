@@ -242,11 +242,6 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void sts4(float* p, float2 a, float2 b) {
-  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "f"(a.x), "f"(a.y), "f"(b.x),
-               "f"(b.y)
-               : "memory");
-}
 __device__ __forceinline__ void sts2(float* p, float2 v) {
   asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(smem_u32(p)), "f"(v.x), "f"(v.y) : "memory");
 }
@@ -266,12 +261,6 @@ __device__ __forceinline__ bool sweep_needs_hdr(const double* stats) {
 #endif
 #ifndef SBF_SWEEP_ACC_BATCH
 #define SBF_SWEEP_ACC_BATCH 0  // accumulate: batched shared-memory reads, clobber-free reds
-#endif
-#ifndef SBF_SWEEP_STS4
-#define SBF_SWEEP_STS4 0  // V phase: one 16-byte shared store per step instead of two 8-byte ones
-#endif
-#ifndef SBF_SWEEP_ITEMS_PER_CTA
-#define SBF_SWEEP_ITEMS_PER_CTA 2  // band height: at least this many items per CTA
 #endif
 #ifndef SBF_SWEEP_ABL
 #define SBF_SWEEP_ABL 0  // phase ablation for timing studies (wrong results when != 0)
@@ -362,7 +351,7 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
   int bandh = p.band;
   {
     const int per_band = max(1, p.nstrips * K_eval);
-    const int nb_min = (SBF_SWEEP_ITEMS_PER_CTA * (int)gridDim.x + per_band - 1) / per_band;
+    const int nb_min = (2 * (int)gridDim.x + per_band - 1) / per_band;
     const int b = (rows_all + nb_min - 1) / nb_min;
     bandh = max(min(b, p.band), min(4 * HALO, p.band));
   }
@@ -525,12 +514,8 @@ __global__ void __launch_bounds__(SweepCfg<R, PASSES>::THREADS, 2)
           const float2 yb = vcascade<J, L, D, PASSES, BORDER>(dB, lB, __fmul2_rn(fx, pk(sv)), a2, nb2, b2, gt);
 #endif
           // VB layout per pixel: [F_c, G_c, F_s, G_s]
-#if SBF_SWEEP_STS4
-          sts4(vdst + J * VBP, ya, yb);
-#else
           sts2(vdst + J * VBP, ya);
           sts2(vdst + J * VBP + 2, yb);
-#endif
         });
       };
 #pragma unroll 1
