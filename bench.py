@@ -52,6 +52,16 @@ E2E_LANES = 3  # streams of the batch API in the e2e leg (copy engine both ways)
 # on B200 (64 config-4 images): 2 lanes 147 ms/step, 3 lanes 125 ms (steady), 4 lanes
 # 125-298 ms (outliers)
 PEAK_FP32_NOMINAL = 148 * 128 * 1.965e9 / 1e12  # T lane-ops/s (FADD/FMUL/FFMA = 1 op)
+def _hbm_peak_gbs():
+    """Measured HBM copy bandwidth of this pool's B200s (MEASURED_PEAKS.json,
+    driver-written), else the profiling recipe's fallback."""
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except Exception:
+        return 6500.0
+
+
 DFMA_PEAK_MEASURED = 16.99  # T DFMA/s on the pool's B200 (profiles/r2_fma_probe.txt)
 DATA = "synthetic (SURVEY.md Appendix A seeded generator; BASELINE names no dataset)"
 
@@ -572,18 +582,81 @@ def run_strips(args, rank, world, dev):
             sf.run()
         e1.record(st)
         e1.synchronize()
-    total, = _max_over_ranks(torch, dev, world, e0.elapsed_time(e1))
+    total = e0.elapsed_time(e1)
     px = 3 * size * size
     plans = sf.plans_host()
+    lib = sf.lib
+
+    # the dominant kernel alone: each channel's split sweep (every term, one
+    # persistent launch) between events on the main stream
+    k3_ms, k3_ops = 0.0, 0.0
+    rows_out = s.out_hi - s.out_lo
+    for c, pl in enumerate(plans):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        b.record(st)  # materialise the handles
+        torch.cuda.synchronize()
+        lib.sbf_set_k3_events(a.cuda_event, b.cuda_event)
+        sf._filter_channel(c, st.cuda_stream, sf.ws, sf.prec)
+        lib.sbf_set_k3_events(None, None)
+        torch.cuda.synchronize()
+        k3_ms += a.elapsed_time(b)
+        k3_ops += OPS_PER_PX_TERM * rows_out * size * (pl.N // 2 - pl.M + 1)
+
+    # end to end through the public strip API with host-resident strips:
+    # page-locked buffer rows in, owned rows out, every byte inside the timed
+    # region (copy engines, per-channel streams)
+    pinned_in = [b.cpu().pin_memory() for b in bufs]
+    pinned_out = [torch.empty((rows_out, size), dtype=b.dtype, pin_memory=True) for b in bufs]
+    sf.run_host(pinned_in, pinned_out)
+    torch.cuda.synchronize()
+    for c in range(3):  # the host results are the device results
+        assert torch.equal(pinned_out[c][:64], sf.out[c][:64].cpu())
+    if world > 1:
+        torch.distributed.barrier()
+    n_e2e = max(1, min(args.steps, 3))
+    e2e_ms = 0.0
+    for _ in range(n_e2e):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        sf.run_host(pinned_in, pinned_out)
+        b.record(st)
+        b.synchronize()
+        e2e_ms += a.elapsed_time(b)
+    h2d = sum(t.numel() * t.element_size() for t in pinned_in)
+    d2h = sum(t.numel() * t.element_size() for t in pinned_out)
+
+    total, e2e_ms, k3_ms_max = _max_over_ranks(torch, dev, world, total, e2e_ms, k3_ms)
     ops = OPS_PER_PX_TERM * size * size * sum(pl.N // 2 - pl.M + 1 for pl in plans)
-    achieved = ops * args.steps / (total * 1e-3) / 1e12
-    peak = PEAK_FP32_NOMINAL * world
+    achieved = k3_ops / (k3_ms * 1e-3) / 1e12
+    traffic = profile_traffic(5)
+    step_ach = ops * args.steps / (total * 1e-3) / 1e12
     return dict(value=px * args.steps / (total * 1e-3) / 1e6, ms_per_step=total / args.steps,
                 launches=sf.launches_per_run() * args.steps, clocks=clk.summary(),
-                roofline=dict(bound="fp32", achieved=achieved, peak=peak, unit="TFLOP/s",
-                              frac=achieved / peak, traffic=profile_traffic(5),
-                              kernel="whole step (K1, plan, term sweeps, epilogue; 3 channels, all ranks)",
-                              ops_basis=f"{OPS_PER_PX_TERM} ops/px/term x {size}^2 px x sum K over channels"),
+                e2e=dict(value=px * n_e2e / (e2e_ms * 1e-3) / 1e6, unit=UNIT,
+                         h2d_bytes_per_step=int(h2d) * world, d2h_bytes_per_step=int(d2h) * world,
+                         ms_per_step=e2e_ms / n_e2e, steps=n_e2e,
+                         path="StripFilter.run_host: page-locked strip rows -> copy-engine H2D per channel, "
+                              "K1, max-allreduce of T, split sweep + K4 per channel, copy-engine D2H of "
+                              "the owned rows into page-locked memory"),
+                roofline=dict(bound="fp32", achieved=achieved, peak=PEAK_FP32_NOMINAL, unit="TFLOP/s",
+                              frac=achieved / PEAK_FP32_NOMINAL, traffic=traffic,
+                              peak_source="nominal 148 SM x 128 FP32 lanes x 1.965 GHz (FADD/FMUL/FFMA = 1 op)",
+                              kernel="split_queue_kernel (SV + SH, every term in one persistent launch), "
+                                     "each channel alone on one stream (CUDA events), this rank's strip",
+                              ops_per_launch=k3_ops / len(plans), k3_ms_per_launch=k3_ms / len(plans),
+                              ops_basis=f"{OPS_PER_PX_TERM} ops/px/term x {rows_out} x {size} px x K_eval per channel",
+                              traffic_source="profiles/k3_traffic_cfg5.json (ncu --set full, one 16384^2 channel)",
+                              hbm=(dict(achieved_gbs=traffic * (rows_out / size) / (k3_ms / len(plans) * 1e-3) / 1e9,
+                                        peak_gbs=_hbm_peak_gbs(),
+                                        frac=traffic * (rows_out / size) / (k3_ms / len(plans) * 1e-3) / 1e9
+                                        / _hbm_peak_gbs(),
+                                        note="measured DRAM traffic of the kernel (not algorithmic bytes) over "
+                                             "its time: the split sweep's U round trip is HBM-heavy")
+                                   if traffic else None)),
+                step_roofline=dict(achieved=step_ach, frac=step_ach / (PEAK_FP32_NOMINAL * world),
+                                   note="whole step (K1, plan, term sweeps, epilogue; 3 channels, all ranks) "
+                                        "against world x nominal peak"),
                 plans=[(pl.T, pl.N, pl.M) for pl in plans])
 
 
