@@ -475,13 +475,15 @@ def run_ours(args, rank, world, dev):
     if world > 1:
         torch.distributed.barrier()
     e2e_ms = 0.0
+    e2e_steps = []
     for _ in range(args.steps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
         res = e2e_call()
         b.record(st)
         b.synchronize()
-        e2e_ms += a.elapsed_time(b)
+        e2e_steps.append(a.elapsed_time(b))
+        e2e_ms += e2e_steps[-1]
         if flush is not None:
             flush.zero_()
     gc.enable()
@@ -536,6 +538,9 @@ def run_ours(args, rank, world, dev):
         launches=KERNELS_PER_IMAGE * len(imgs) * args.steps,
         e2e=dict(value=e2e_value, unit=UNIT, h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h),
                  ms_per_step=e2e_ms / args.steps,
+                 # this rank's steps: PCIe-bound legs show host-side outliers here
+                 ms_step_min_median_max=[float(np.min(e2e_steps)), float(np.median(e2e_steps)),
+                                         float(np.max(e2e_steps))],
                  path=(f"shiftable_bf_batch ({E2E_LANES} streams): pinned host images -> copy-engine H2D, "
                        "kernels, copy-engine D2H of each result into pinned host memory; "
                        "both PCIe directions overlap other images' kernels") if cfg == 4 else
