@@ -642,8 +642,9 @@ def run_strips(args, rank, world, dev):
                          h2d_bytes_per_step=int(h2d) * world, d2h_bytes_per_step=int(d2h) * world,
                          ms_per_step=e2e_ms / n_e2e, steps=n_e2e,
                          path="StripFilter.run_host: page-locked strip rows -> copy-engine H2D per channel, "
-                              "K1, max-allreduce of T, split sweep + K4 per channel, copy-engine D2H of "
-                              "the owned rows into page-locked memory"),
+                              "K1 and a max-allreduce of T per channel, split sweep + K4, copy-engine D2H "
+                              "of the owned rows into page-locked memory; channel c's sweep overlaps "
+                              "channel c+1's upload and channel c-1's download"),
                 roofline=dict(bound="fp32", achieved=achieved, peak=PEAK_FP32_NOMINAL, unit="TFLOP/s",
                               frac=achieved / PEAK_FP32_NOMINAL, traffic=traffic,
                               peak_source="nominal 148 SM x 128 FP32 lanes x 1.965 GHz (FADD/FMUL/FFMA = 1 op)",

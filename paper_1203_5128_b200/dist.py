@@ -174,46 +174,60 @@ class StripFilter:
         """run() for strips that live in host memory: `host_bufs[c]` (this
         rank's buffer rows of channel c, ideally page-locked) is copied to the
         device, filtered, and the owned rows are copied into `host_outs[c]`.
-        Copies ride the copy engines on per-channel streams: channel c+1's
-        upload overlaps channel c's K1, and (overlap mode) each channel's
-        download starts as soon as its own K3/K4 is done.  Stream-ordered on
-        `stream_ptr`; call check() (or synchronise) before reading the host
-        results."""
+        The channels are pipelined: uploads and downloads ride the copy
+        engines on per-channel streams, and every channel reduces its own T
+        (one small collective per channel instead of one for all), so channel
+        c's sweep overlaps channel c+1's upload and channel c-1's download.
+        Stream-ordered on `stream_ptr`; call check() (or synchronise) before
+        reading the host results."""
         import torch
         main = self._stream_obj(stream_ptr)
         if not hasattr(self, "copy_streams"):
             self.copy_streams = [torch.cuda.Stream(device=self.dev) for _ in self.bufs]
         start = torch.cuda.Event()
         start.record(main)
-        lib, s = self.lib, self.strip
+        lib, s, p = self.lib, self.strip, self.params
         st = self._stream(stream_ptr)
         lo, hi = s.out_lo - s.buf_lo, s.out_hi - s.buf_lo
-        use_fixed = self.params.fixed_T is not None
+        use_fixed = p.fixed_T is not None
         ups = []
         for c, cs in enumerate(self.copy_streams):
-            cs.wait_event(start)  # the previous run's kernels are done with bufs[c]
+            cs.wait_event(start)  # the previous run's kernels are done with bufs[c] / out[c]
             with torch.cuda.stream(cs):
                 self.bufs[c].copy_(host_bufs[c], non_blocking=True)
             e = torch.cuda.Event()
             e.record(cs)
             ups.append(e)
+        with torch.cuda.stream(main):
+            self.fb.zero_()
         for c, b in enumerate(self.bufs):
             main.wait_event(ups[c])
             _lib.check(lib.sbf_local_range(b.data_ptr(), self.dt[c], self.H, self.W, self.W,
                                            0 if use_fixed else self.R, lo, hi, None,
                                            self.stats[c].data_ptr(), self.ws.data_ptr(),
                                            self.ws.numel(), st), "local_range")
-        with torch.cuda.stream(main):
-            self.T.copy_(self.stats[:, 0])
-            if not use_fixed:
-                self.reduce_max(self.T)
-        self.finish(stream_ptr=stream_ptr, host_outs=host_outs)
+            with torch.cuda.stream(main):
+                self.T[c:c + 1].copy_(self.stats[c, 0:1])
+                if not use_fixed:
+                    self.reduce_max(self.T[c:c + 1])
+            _lib.check(lib.sbf_plan_device(
+                self.T[c:c + 1].data_ptr(), 1 if use_fixed else 0,
+                float(p.fixed_T) if use_fixed else 0.0, float(p.sigma_r), float(p.epsilon),
+                _lib.RULES[p.truncation], log_2_over_eps(p.epsilon), self.plans[c].data_ptr(),
+                self.terms[c].data_ptr(), TERMS_CAP, st), "plan")
+            self._filter_channel(c, st, self.ws, self.prec)
+            done = torch.cuda.Event()
+            done.record(main)
+            cs = self.copy_streams[c]
+            cs.wait_event(done)
+            with torch.cuda.stream(cs):
+                host_outs[c].copy_(self.out[c], non_blocking=True)
+        for cs in self.copy_streams:
+            main.wait_stream(cs)
         return host_outs
 
-    def finish(self, T_global=None, stream_ptr=None, host_outs=None):
-        """K2/K3/K4 per channel with the global T (device tensor, per channel);
-        `host_outs`: also copy each channel's owned rows to host memory behind
-        its own kernels."""
+    def finish(self, T_global=None, stream_ptr=None):
+        """K2/K3/K4 per channel with the global T (device tensor, per channel)."""
         lib, s = self.lib, self.strip
         st = self._stream(stream_ptr)
         lo, hi = s.out_lo - s.buf_lo, s.out_hi - s.buf_lo
@@ -238,11 +252,6 @@ class StripFilter:
                 _lib.RULES[p.truncation], log_2_over_eps(p.epsilon), self.plans[c].data_ptr(),
                 self.terms[c].data_ptr(), TERMS_CAP, cst), "plan")
             self._filter_channel(c, cst, ws, self.prec)
-            if host_outs is not None:
-                import torch
-                cso = self.side[c] if self.overlap else self._stream_obj(stream_ptr)
-                with torch.cuda.stream(cso):
-                    host_outs[c].copy_(self.out[c], non_blocking=True)
         if self.overlap:
             for c in range(len(self.bufs)):
                 e = torch.cuda.Event()

@@ -454,6 +454,19 @@ def test_strip_filter_run_host_matches_run(overlap):
     params = P.FilterParams(sigma_s=12.0, sigma_r=15.0, epsilon=0.01, precision="fp32")
     full = [P.shiftable_bf(ch, params) for ch in chans]
     strips = strip_plan(320, 2, strip_halo(params))
+    Ts = [f.plan.T for f in full]
+
+    class GlobalT:  # stands in for the max all-reduce: all channels at once, or one by one
+        def __init__(self):
+            self.i = 0
+
+        def __call__(self, t):
+            if t.numel() == len(Ts):
+                t.copy_(torch.tensor(Ts, device=t.device))
+            else:
+                t.fill_(Ts[self.i % len(Ts)])
+                self.i += 1
+
     outs = [[], []]
     for s in strips:
         host_in = [torch.from_numpy(np.ascontiguousarray(ch[s.buf_lo:s.buf_hi])).pin_memory() for ch in chans]
@@ -461,11 +474,10 @@ def test_strip_filter_run_host_matches_run(overlap):
         dev_in = [t.cuda() for t in host_in]
         # the device buffers are refilled by run_host: start from garbage
         sf = StripFilter([torch.full_like(t, 7.0) for t in dev_in], s, 320, params, overlap=overlap,
-                         reduce_max=lambda t: t.copy_(torch.tensor([f.plan.T for f in full], device=t.device)))
+                         reduce_max=GlobalT())
         sf.run_host(host_in, host_out)
         sf.check()
-        ref = StripFilter(dev_in, s, 320, params,
-                          reduce_max=lambda t: t.copy_(torch.tensor([f.plan.T for f in full], device=t.device)))
+        ref = StripFilter(dev_in, s, 320, params, reduce_max=GlobalT())
         ref.run()
         torch.cuda.synchronize()
         for c in range(2):
