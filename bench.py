@@ -42,7 +42,9 @@ sys.path.insert(0, REPO)
 # our kernels per filtered image (fused pipeline): row max (+ statistics
 # reset), column max (+ ticket clear, plan in its last CTA), K3 term sweep
 # (+ divide / fallback epilogue)
-KERNELS_PER_IMAGE = 3
+# kernels of this repo that one fused call launches, per image (ncu launch lists of one
+# step: profiles/r2_step_launches_cfg<N>.csv; config 5 counts in StripFilter.launches_per_run)
+KERNELS_PER_IMAGE = {1: 5, 2: 4, 3: 9, 4: 8}
 METRIC = "Mpixel/s shiftable Gaussian BF at 1/2/4/8 B200; % of FP32/HBM roofline"
 UNIT = "Mpixel/s"
 OPS_PER_PX_TERM = 132   # phasor 4 + f*c,f*s 2 + 4 images x 6 line passes x 5 + acc 6
@@ -535,7 +537,7 @@ def run_ours(args, rank, world, dev):
                         note="132 ops/px/term x K_eval of the term sweeps it replaces"))
     return dict(
         value=value, ms_per_step=step_ms / args.steps, clocks=clk.summary(),
-        launches=KERNELS_PER_IMAGE * len(imgs) * args.steps,
+        launches=KERNELS_PER_IMAGE[cfg] * len(imgs) * args.steps,
         e2e=dict(value=e2e_value, unit=UNIT, h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h),
                  ms_per_step=e2e_ms / args.steps,
                  # this rank's steps: PCIe-bound legs show host-side outliers here

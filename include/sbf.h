@@ -189,7 +189,7 @@ int sbf_filter(const void* f, int dtype, int64_t H, int64_t W, int64_t ld,
 
 /* Whole pipeline (K1 -> K2 -> K3 -> K4) on device buffers.  No host sync
  * and CUDA-graph capturable on the fp32 paths (the K3 sweep, r <= 5, and the
- * split sweep, r >= 9, with SBF_PREC_FP32 / SBF_PREC_AUTO).  The fp64 paths
+ * split sweep, 6 <= r <= 12, with SBF_PREC_FP32 / SBF_PREC_AUTO).  The fp64 paths
  * (SBF_PREC_HDR, radii without an fp32 kernel) read the plan on the host to
  * size their term loop / pick the dual form: they synchronise the stream
  * and return SBF_ERR_UNSUPPORTED under graph capture.

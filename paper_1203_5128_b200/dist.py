@@ -307,14 +307,13 @@ class StripFilter:
         return out
 
     def launches_per_run(self):
-        """Kernels one run() launches: per channel K1 (row + column pass), the
-        plan, and the filter (K3 + epilogue, or two sweeps per term and the
-        epilogue on the split path for radii >= 9)."""
-        n = 0
-        for pl in self.plans_host():
-            K = pl.N // 2 - pl.M + 1
-            n += 3 + (2 * K + 1 if self.sp.r >= 9 else 2)
-        return n
+        """Kernels of this library one run() launches (fp32 paths): per channel
+        K1 (pruned exact T on strips of at least 4 Mpx: init, tile pass,
+        bounds, two exact rounds, final; else the two line passes), the plan,
+        and the filter (K3 sweep + divide, or the persistent split sweep + K4)
+        -- profiles/r2_step_launches_cfg5.csv."""
+        k1 = 6 if self.H * self.W >= (4 << 20) and self.R <= 48 else 2
+        return len(self.bufs) * (k1 + 1 + 2)
 
     def _filter_channel(self, c, st, ws, prec):
         s = self.strip
