@@ -469,8 +469,12 @@ def run_ours(args, rank, world, dev):
         # into page-locked memory by the K3 epilogue)
         return [P.shiftable_bf(pinned_in[0], params)]
 
-    for _ in range(max(1, min(args.warmup, 2))):
-        e2e_call()
+    # warm-up as the timed loop runs: the previous result stays alive while the
+    # next call allocates its page-locked output (two blocks of the caching
+    # host allocator in rotation; a first-time cudaHostAlloc costs milliseconds)
+    res = None
+    for _ in range(max(2, min(args.warmup, 3))):
+        res = e2e_call()
     torch.cuda.synchronize()
     gc.collect()
     gc.disable()  # no collector pauses inside the timed region
