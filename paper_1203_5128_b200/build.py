@@ -24,7 +24,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-Xptxas", "-warn-spills", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-I", INCLUDE, "-I", CSRC]
+         "-I", INCLUDE, "-I", CSRC] + os.environ.get("SBF_NVCC_FLAGS", "").split()
 
 SOURCES = ["sbf_api.cu", "sbf_plan.cu", "sbf_local_range.cu", "sbf_generic.cu", "sbf_pgm.cu",
            "sbf_direct.cu", "sbf_nlm.cu", "sbf_dual.cu", "sbf_smooth.cu", "sbf_stage.cu"]
