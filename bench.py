@@ -735,7 +735,8 @@ def main():
     line = dict(metric=METRIC, value=r["value"], unit=UNIT, n_gpus=world, steps=args.steps,
                 warmup=args.warmup, ms_per_step=r["ms_per_step"], higher_is_better=True,
                 scaling="strong" if args.config in (4, 5) else "weak", vs_baseline=None,
-                dtype="f32", data=DATA, config=cfgd, roofline=r["roofline"], cpu_baseline=cpu,
+                dtype="f64" if args.config == 3 else "f32",  # the arithmetic type of the dominant kernel
+                data=DATA, config=cfgd, roofline=r["roofline"], cpu_baseline=cpu,
                 e2e=r.get("e2e"), gpu_launches=r["launches"], clocks=r["clocks"])
     for k in ("step_roofline", "plans"):
         if k in r:
