@@ -47,7 +47,9 @@ def split_instantiations(kind: str):
     """(r, passes) pairs with a split-sweep (SV/SH) instantiation."""
     if kind == "min":
         return [(5, 3)]
-    return [(r, 3) for r in range(5, 13)]
+    # (single-pass boxes of radius 6..12 too: every fp32 radius >= 6 is then
+    # served by the bit-reproducible split sweep)
+    return [(r, 3) for r in range(5, 13)] + [(r, 1) for r in range(6, 13)]
 
 
 def sweep_instantiations(kind: str):

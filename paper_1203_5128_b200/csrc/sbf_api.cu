@@ -55,10 +55,13 @@ static const SplitEntry* find_split(const sbf_spatial& sp, int precision) {
 #include "sbf_split_list.inc"
 #undef SBF_Y
   };
-  if (precision != SBF_PREC_FP32 || g_split_min_r <= 0 || sp.mode == SBF_SPATIAL_BOX) return nullptr;
-  if (sp.r < g_split_min_r || !(sp.alpha <= 0.999)) return nullptr;
+  if (precision != SBF_PREC_FP32 || g_split_min_r <= 0) return nullptr;
+  if (sp.mode != SBF_SPATIAL_BOX && sp.mode != SBF_SPATIAL_ITERATED) return nullptr;
+  const bool box = sp.mode == SBF_SPATIAL_BOX;  // one pass, alpha = 0
+  if (sp.r < g_split_min_r || (!box && !(sp.alpha <= 0.999))) return nullptr;
+  const int passes = box ? 1 : sp.passes;
   for (const auto& e : reg)
-    if (e.r == sp.r && e.passes == sp.passes) return &e;
+    if (e.r == sp.r && e.passes == passes) return &e;
   return nullptr;
 }
 

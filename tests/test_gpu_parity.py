@@ -407,6 +407,32 @@ def test_split_sweep_matches_strip_kernel_and_oracle(shape, sigma_s, sigma_r):
     assert float(np.abs(outs[0] - outs[1]).max()) < 5e-3
 
 
+@pytest.mark.parametrize("shape,radius", [((200, 300), 7), ((97, 410), 12), ((64, 64), 6)])
+def test_single_pass_box_large_radius_split_sweep(shape, radius):
+    """Box(r) with r = 6..12 runs the split sweep (one pass, alpha = 0): it
+    matches the oracle, is bit-reproducible across calls, and agrees with the
+    round-1 term kernel (split sweep off) where that kernel can run."""
+    lib = _lib.load()
+    img = np.random.default_rng(radius).uniform(0, 255, shape).astype(np.float32)
+    params = P.FilterParams(sigma_s=float(radius), sigma_r=30.0, epsilon=0.01, spatial=P.Box(radius),
+                            precision="fp32")
+    ref = O.shiftable_bf(img, float(radius), 30.0, 0.01, spatial=("box", radius))
+    res = P.shiftable_bf(img, params)
+    assert (res.plan.T, res.plan.N, res.plan.M) == (ref["T"], ref["N"], ref["M"])
+    assert_close_image(res.image, ref["image"])
+    assert np.array_equal(P.shiftable_bf(img, params).image, res.image)
+    if radius > 8:
+        return  # (the round-1 term kernel's single-pass instantiations need more shared memory than an SM has there)
+    try:
+        assert lib.sbf_set_split_min_radius(0) == 0
+        P.bilateral._workspace_layout.cache_clear()
+        old = P.shiftable_bf(img, params)
+    finally:
+        lib.sbf_set_split_min_radius(-1)
+        P.bilateral._workspace_layout.cache_clear()
+    assert float(np.abs(old.image - res.image).max()) < 5e-3
+
+
 @pytest.mark.parametrize("shape,sigma_s,sigma_r,dtype", [
     ((300, 517), 2.0, 25.0, "float32"), ((777, 1031), 4.0, 30.0, "float32"),
     ((130, 260), 1.0, 25.0, "float64"), ((64, 3000), 6.0, 20.0, "float32"),
