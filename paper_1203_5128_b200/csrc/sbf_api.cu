@@ -47,6 +47,11 @@ int launch_generic_terms(const FilterLaunch& a, double* nd);
 // 3.12 / 3.19 ms vs the round-1 term kernel 3.16 / 3.38 ms, and the split sweep
 // is bit-reproducible)
 #define SBF_SPLIT_MIN_R_DEFAULT 6
+// (round 1 kept fractional weights above 0.999 on the term kernel; the split
+// sweep matches the oracle there too: tests/test_gpu_parity.py, alpha = 0.9992)
+#ifndef SBF_SPLIT_ALPHA_MAX
+#define SBF_SPLIT_ALPHA_MAX 1.0
+#endif
 static thread_local int g_split_min_r = SBF_SPLIT_MIN_R_DEFAULT;
 
 static const SplitEntry* find_split(const sbf_spatial& sp, int precision) {
@@ -58,7 +63,7 @@ static const SplitEntry* find_split(const sbf_spatial& sp, int precision) {
   if (precision != SBF_PREC_FP32 || g_split_min_r <= 0) return nullptr;
   if (sp.mode != SBF_SPATIAL_BOX && sp.mode != SBF_SPATIAL_ITERATED) return nullptr;
   const bool box = sp.mode == SBF_SPATIAL_BOX;  // one pass, alpha = 0
-  if (sp.r < g_split_min_r || (!box && !(sp.alpha <= 0.999))) return nullptr;
+  if (sp.r < g_split_min_r || (!box && !(sp.alpha <= SBF_SPLIT_ALPHA_MAX))) return nullptr;
   const int passes = box ? 1 : sp.passes;
   for (const auto& e : reg)
     if (e.r == sp.r && e.passes == passes) return &e;

@@ -407,6 +407,25 @@ def test_split_sweep_matches_strip_kernel_and_oracle(shape, sigma_s, sigma_r):
     assert float(np.abs(outs[0] - outs[1]).max()) < 5e-3
 
 
+@pytest.mark.parametrize("sigma_s,r", [(7.4826, 6), (10.4874, 9), (11.4885, 10)])
+def test_split_sweep_fractional_weight_near_one(sigma_s, r):
+    """3-pass radii >= 6 whose fractional weight alpha is just below 1
+    (alpha > 0.999: almost a box of radius r + 1) run the split sweep like
+    every other radius >= 6: oracle parity and bit-reproducibility."""
+    from paper_1203_5128_b200.spatial import to_c_spatial
+    img = np.random.default_rng(3).uniform(0, 255, (200, 333)).astype(np.float32)
+    img[80:, 150:] += 30
+    img = np.clip(img, 0, 255)
+    params = P.FilterParams(sigma_s=sigma_s, sigma_r=25.0, epsilon=0.01, precision="fp32")
+    sp = to_c_spatial(params.resolved_spatial())
+    assert sp.r == r and sp.alpha > 0.999
+    ref = O.shiftable_bf(img.astype(np.float64), sigma_s, 25.0, 0.01)
+    res = P.shiftable_bf(img, params)
+    assert (res.plan.T, res.plan.N, res.plan.M) == (ref["T"], ref["N"], ref["M"])
+    assert_close_image(res.image, ref["image"])
+    assert np.array_equal(P.shiftable_bf(img, params).image, res.image)
+
+
 @pytest.mark.parametrize("shape,radius", [((200, 300), 7), ((97, 410), 12), ((64, 64), 6)])
 def test_single_pass_box_large_radius_split_sweep(shape, radius):
     """Box(r) with r = 6..12 runs the split sweep (one pass, alpha = 0): it
