@@ -134,10 +134,12 @@ def _read_meta(meta):
     return buf.numpy().copy()
 
 
-@functools.lru_cache(maxsize=64)
 def _workspace_layout(H, W, dtype, sp_key, prec):
     """(total bytes, term-table offset, filter-workspace offset) of the
-    sbf_shiftable_bf workspace: [K1 workspace | term table | K3/K4 workspace]."""
+    sbf_shiftable_bf workspace: [K1 workspace | term table | K3/K4 workspace].
+    Asked of the library on every call (two cheap C calls): the answer depends
+    on the library's thread-local path switches (sbf_set_split_min_radius ...),
+    so it must not be memoised here."""
     lib = _lib.load()
     sp = _lib.SbfSpatial(*sp_key)
     total = lib.sbf_shiftable_bf_workspace(H, W, dtype, sp, prec, TERMS_CAP)

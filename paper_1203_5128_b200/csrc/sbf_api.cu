@@ -49,6 +49,9 @@ int launch_generic_terms(const FilterLaunch& a, double* nd);
 #define SBF_SPLIT_MIN_R_DEFAULT 6
 // (round 1 kept fractional weights above 0.999 on the term kernel; the split
 // sweep matches the oracle there too: tests/test_gpu_parity.py, alpha = 0.9992)
+#ifndef SBF_SPLIT_MAX_SEG
+#define SBF_SPLIT_MAX_SEG 4096
+#endif
 #ifndef SBF_SPLIT_ALPHA_MAX
 #define SBF_SPLIT_ALPHA_MAX 1.0
 #endif
@@ -546,7 +549,12 @@ static int launch_split_path(const FilterLaunch& a, const SplitEntry& se, int r,
   p.band = (p.band + 31) / 32 * 32;  // whole SH row groups per band
   const int64_t rgroups = (rows_out + se.sh_rows - 1) / se.sh_rows;
   const int64_t ns = smax<int64_t>(1, (want + rgroups - 1) / rgroups);
-  p.seg = (int)smax<int64_t>(16 * halo, (a.W + ns - 1) / ns);
+  // SH streams at most SBF_SPLIT_MAX_SEG columns from one zero state: the fp32
+  // running sums drift with the stream length (full-width rows measured 1.0e-3 /
+  // 1.5e-3 / 3.8e-3 gray levels at W = 8192 / 16384 / 32768 against 2e-4 at the
+  // start of a row); each segment re-warms over 2 * halo columns
+  p.seg = (int)smin<int64_t>(smax<int64_t>(16 * halo, (a.W + ns - 1) / ns),
+                             smax<int64_t>(16 * halo, SBF_SPLIT_MAX_SEG));
   p.svx = (int)cgroups;
   p.svy = (int)((rows_out + p.band - 1) / p.band);
   p.shx = (int)rgroups;

@@ -444,11 +444,9 @@ def test_single_pass_box_large_radius_split_sweep(shape, radius):
         return  # (the round-1 term kernel's single-pass instantiations need more shared memory than an SM has there)
     try:
         assert lib.sbf_set_split_min_radius(0) == 0
-        P.bilateral._workspace_layout.cache_clear()
         old = P.shiftable_bf(img, params)
     finally:
         lib.sbf_set_split_min_radius(-1)
-        P.bilateral._workspace_layout.cache_clear()
     assert float(np.abs(old.image - res.image).max()) < 5e-3
 
 

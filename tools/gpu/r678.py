@@ -12,7 +12,6 @@ for ss in (7.0, 8.0, 9.5):
     outs = {}
     for mr in (9, 6):
         lib.sbf_set_split_min_radius(mr)
-        P.bilateral._workspace_layout.cache_clear()
         for _ in range(2): res = P.shiftable_bf(img, params)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
