@@ -9,7 +9,6 @@ GPU as K1 (local range) -> K2 (plan on device) -> K3 (fused term kernel)
 
 from __future__ import annotations
 
-import functools
 import threading
 import warnings
 from dataclasses import dataclass
