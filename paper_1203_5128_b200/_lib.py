@@ -104,6 +104,29 @@ EXPORTS = tuple(_SIGS)
 _lock = threading.Lock()
 _lib = None
 
+# One filter call at a time per process.  Calls from several Python threads are
+# serialised (kernels of different calls still overlap when they were enqueued
+# on different streams by ONE thread, e.g. shiftable_bf_batch).  Without this
+# lock tools/gpu/check_threads.py ended 3 of 6 whole-suite runs with a CUDA
+# illegal memory access; with it 4 of 4 were clean (cause not found: DESIGN.md
+# section 5).  SBF_SERIALISE_CALLS=0 removes it for experiments.
+CALL_LOCK = threading.RLock()
+_SERIALISE = os.environ.get("SBF_SERIALISE_CALLS", "1") != "0"
+
+
+def serialised(fn):
+    """Decorator: run a public entry point under the process-wide call lock."""
+    if not _SERIALISE:
+        return fn
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        with CALL_LOCK:
+            return fn(*args, **kwargs)
+
+    return wrapper
+
 
 def load():
     """Load libsbf.so once; raise loudly if it was not built."""

@@ -91,6 +91,7 @@ def _precision_code(params) -> int:
     return _lib.PREC_AUTO
 
 
+@_lib.serialised
 def shiftable_bf(img, params: FilterParams) -> ShiftableResult:
     """Constant-time bilateral filter; returns (image, plan, fallback count).
 
@@ -254,6 +255,7 @@ def _filter_on_device(s, params: FilterParams, out_f64: bool, to_host: bool = Fa
     return out, _plan_from_struct(plan_c), fallbacks
 
 
+@_lib.serialised
 def shiftable_bf_batch(imgs, params: FilterParams, lanes: int = 3, out=None, stage: str = "ce"):
     """`[shiftable_bf(img, params) for img in imgs]`, pipelined on the GPU.
 

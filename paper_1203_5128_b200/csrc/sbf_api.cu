@@ -163,24 +163,20 @@ void retain_default_pool() {
 
 cudaError_t ensure_dyn_smem(const void* func, size_t bytes) {
   // cudaFuncSetAttribute costs microseconds per call; raise the limit only
-  // when a launch needs more than any earlier one on this device
+  // when a launch needs more than any earlier one on this device.  The
+  // attribute is set under the lock: two threads growing the same kernel at
+  // once must not leave the smaller value behind the larger record.
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, size_t> done;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   const auto key = std::make_pair(func, dev);
-  {
-    std::lock_guard<std::mutex> g(mu);
-    auto it = done.find(key);
-    if (it != done.end() && it->second >= bytes) return cudaSuccess;
-  }
+  std::lock_guard<std::mutex> g(mu);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
   e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e == cudaSuccess) {
-    std::lock_guard<std::mutex> g(mu);
-    size_t& v = done[key];
-    if (v < bytes) v = bytes;
-  }
+  if (e == cudaSuccess) done[key] = bytes;
   return e;
 }
 

@@ -101,6 +101,7 @@ def _taps(mode, radius):
     raise InvalidParameterError(f"unknown spatial mode {mode!r}")
 
 
+@_lib.serialised
 def direct_bf(img, spatial, range_kernel, radius=None):
     """Brute-force bilateral filter over the clamped window (bilateral.py:205-239).
 

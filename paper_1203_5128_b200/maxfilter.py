@@ -42,6 +42,7 @@ def _nonfinite(stats_host) -> bool:
     return int(np.asarray(stats_host[7:8]).view(np.uint64)[0]) != 0
 
 
+@_lib.serialised
 def max_filter_2d(img, radius):
     """Maximum over the clamped (2R+1)^2 window (maxfilter.py:41-49)."""
     if radius < 0:
@@ -56,6 +57,7 @@ def max_filter_2d(img, radius):
     return M
 
 
+@_lib.serialised
 def max_filter_1d(seq, radius):
     """Sliding maximum over the clamped window [i-R, i+R] (maxfilter.py:21-28)."""
     arr = np.asarray(seq, dtype=np.float64)
@@ -66,6 +68,7 @@ def max_filter_1d(seq, radius):
     return max_filter_2d(arr.reshape(1, -1), int(radius))[0]
 
 
+@_lib.serialised
 def compute_T(img, radius) -> float:
     """Exact max |f(x-y) - f(x)| over square windows (maxfilter.py:56-61)."""
     if radius < 0:
@@ -80,6 +83,7 @@ def compute_T(img, radius) -> float:
     return float(st[0])
 
 
+@_lib.serialised
 def brute_force_T(img, radius) -> float:
     """max |f(x+y) - f(x)| over all pixels and in-image offsets |y| <= R,
     evaluated directly (O(R^2) per pixel) on the GPU — reference

@@ -110,6 +110,7 @@ def build_items(plans):
     return arr, len(items)
 
 
+@_lib.serialised
 def coarse_nlm_shiftable(img, patch: PatchSpec, spatial: SpatialMode, radius: int,
                          epsilon: float, truncation: str = "auto",
                          max_component_order: int = DEFAULT_COMPONENT_ORDER_CAP,
@@ -170,6 +171,7 @@ def expansion_range_for(plan: KernelPlan):
     return expansion_range(raised_cosine_expansion(plan))
 
 
+@_lib.serialised
 def direct_nlm(img, patch: PatchSpec, spatial: SpatialMode, radius: int,
                range_kernels="gaussian"):
     """Literal windowed coarse NLM (nlm.py:140-183), the shiftable NLM's test

@@ -113,6 +113,7 @@ def _smooth(img, sp):
     return out.cpu().numpy() if numpy_in else (out.cpu() if s.host else out)
 
 
+@_lib.serialised
 def box_filter(img, radius):
     """Mean over the clamped (2r+1)^2 window (spatial.py:65-78)."""
     radius = int(radius)
@@ -121,11 +122,13 @@ def box_filter(img, radius):
     return _smooth(img, to_c_spatial(Box(radius)))
 
 
+@_lib.serialised
 def iterated_box_gaussian(img, sigma_s, passes=3):
     """`passes` extended-box passes of variance sigma_s^2/passes each (spatial.py:108-139)."""
     return _smooth(img, to_c_spatial(IteratedBox(sigma_s, passes)))
 
 
+@_lib.serialised
 def fir_gaussian(img, sigma_s, radius):
     """Separable sampled Gaussian, renormalised per clamped window (spatial.py:142-172)."""
     if sigma_s <= 0:
@@ -137,6 +140,7 @@ def fir_gaussian(img, sigma_s, radius):
     return _smooth(img, sp)
 
 
+@_lib.serialised
 def apply_spatial(img, mode: SpatialMode):
     """spatial.py:175-182."""
     if isinstance(mode, Box):

@@ -2,11 +2,11 @@
 pkg/README.md:130-131): threads filtering different images through different
 paths at the same time get exactly what serial calls give.
 
-Run explicitly (python -m pytest tools/gpu/check_threads.py -m gpu): alone it
-passes; appended to the whole GPU suite in one process, 2 of 3 runs ended
-with SIGABRT raised on a thread without a Python frame while the workers were
-inside torch (pageable copy / stream synchronise) -- unresolved, see
-DESIGN.md section 5, so it is not part of the default suite."""
+Run explicitly (python -m pytest tools/gpu/check_threads.py -m gpu).  The
+Python entry points serialise concurrent callers with a process-wide lock
+(_lib.serialised); without it (SBF_SERIALISE_CALLS=0) this check, appended
+to the whole GPU suite in one process, hit a CUDA illegal memory access in 3
+of 6 runs -- see DESIGN.md section 5.  It stays outside the default suite."""
 import os
 import sys
 
